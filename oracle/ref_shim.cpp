@@ -1,0 +1,182 @@
+// TEST/BASELINE INFRASTRUCTURE ONLY — C entry points onto the UNMODIFIED
+// reference library (/root/reference/proj/src/*.cpp), compiled from where
+// the sources lie by oracle/Makefile into oracle/_ref/libsfref.so.
+//
+// Used to (1) pin the C oracle restatement against the reference's own
+// distributed CPU path on identical graphs and data, (2) generate golden
+// fixtures (tests/golden/make_golden.py), and (3) time the reference CPU
+// path for bench.py's reference arm / cpu_baseline. Never used by the
+// product package.
+//
+// Everything here calls the reference's public API: sf::run_ranks
+// (harness.hpp:58-72), StarForest::set_graph/setup (starforest.hpp:71-79)
+// and the ops in ops.hpp:57-94.
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "sf/harness.hpp"
+#include "sf/ops.hpp"
+#include "sf/starforest.hpp"
+
+namespace {
+thread_local std::string g_err;
+
+sf::GraphSpec make_spec(int r, const int64_t* nroots, const int64_t* nleaves,
+                        const int64_t* const* local, const int32_t* const* rrank,
+                        const int64_t* const* roff) {
+  sf::GraphSpec s;
+  s.nroots = nroots[r];
+  s.nleaves = nleaves[r];
+  if (local && local[r]) s.local = std::vector<int64_t>(local[r], local[r] + nleaves[r]);
+  s.remote.resize(static_cast<size_t>(nleaves[r]));
+  for (int64_t i = 0; i < nleaves[r]; ++i) s.remote[static_cast<size_t>(i)] = sf::RootRef{rrank[r][i], roff[r][i]};
+  return s;
+}
+}  // namespace
+
+extern "C" {
+
+const char* sfref_last_error() { return g_err.c_str(); }
+
+// opkind: 0 bcast(a=root in, b=leaf inout), 1 reduce(a=leaf in, b=root inout),
+// 2 fetch_and_op(a=root inout, b=leaf in, c=leafupdate inout),
+// 3 gather(a=leaf in, b=multiroot out), 4 scatter(a=multiroot in, b=leaf inout)
+int sfref_run(int nranks, const int64_t* nroots, const int64_t* nleaves,
+              const int64_t* const* local, const int32_t* const* rrank,
+              const int64_t* const* roff, int opkind, int kind, int64_t blocklen, int op,
+              int deterministic, int force_remote, uint64_t seed, void* const* a, void* const* b,
+              void* const* c) {
+  try {
+    sf::RunConfig cfg;
+    cfg.nranks = nranks;
+    cfg.deterministic = deterministic != 0;
+    cfg.force_remote = force_remote != 0;
+    cfg.seed = seed;
+    cfg.timeout_s = 60.0;
+    const sf::Unit u{static_cast<sf::Kind>(kind), blocklen};
+    const auto rop = static_cast<sf::ReduceOp>(op);
+    sf::run_ranks(cfg, [&](sf::Comm& comm) {
+      const int r = comm.rank();
+      sf::StarForest f(comm);
+      f.set_graph(make_spec(r, nroots, nleaves, local, rrank, roff));
+      f.setup();
+      switch (opkind) {
+        case 0: sf::bcast(f, u, a[r], b[r], rop); break;
+        case 1: sf::reduce(f, u, a[r], b[r], rop); break;
+        case 2: sf::fetch_and_op(f, u, a[r], b[r], c[r], rop); break;
+        case 3: sf::gather(f, u, a[r], b[r]); break;
+        case 4: sf::scatter(f, u, a[r], b[r]); break;
+        default: throw sf::Error("unknown opkind");
+      }
+    });
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// Two-sided info of every rank (starforest.hpp:47-55) flattened as
+// [ngroups, (rank, n, items...)...] for root groups then leaf groups.
+int sfref_two_sided(int nranks, const int64_t* nroots, const int64_t* nleaves,
+                    const int64_t* const* local, const int32_t* const* rrank,
+                    const int64_t* const* roff, int64_t* const* out, const int64_t* out_cap) {
+  try {
+    sf::RunConfig cfg;
+    cfg.nranks = nranks;
+    sf::run_ranks(cfg, [&](sf::Comm& comm) {
+      const int r = comm.rank();
+      sf::StarForest f(comm);
+      f.set_graph(make_spec(r, nroots, nleaves, local, rrank, roff));
+      f.setup();
+      std::vector<int64_t> v;
+      const auto& ti = f.two_sided();
+      for (const auto* gs : {&ti.root_ranks, &ti.leaf_ranks}) {
+        v.push_back(static_cast<int64_t>(gs->size()));
+        for (const auto& g : *gs) {
+          v.push_back(g.rank);
+          v.push_back(static_cast<int64_t>(g.items.size()));
+          v.insert(v.end(), g.items.begin(), g.items.end());
+        }
+      }
+      if (static_cast<int64_t>(v.size()) > out_cap[r]) throw sf::Error("two_sided: output too small");
+      std::memcpy(out[r], v.data(), v.size() * sizeof(int64_t));
+    });
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// Time `steps` iterations of Bcast(REPLACE) + Reduce(SUM) on float64 data
+// over the given graph with the reference's threads backend (one thread per
+// rank, single-threaded per rank by design). Timing per rank with
+// steady_clock between barriers; out[0] = max SetUp seconds, out[1] = max over
+// ranks of mean microseconds per step, out[2] = mean bcast us, out[3] = mean
+// reduce us (rank 0).
+int sfref_time_bcast_reduce(int nranks, const int64_t* nroots, const int64_t* nleaves,
+                            const int64_t* const* local, const int32_t* const* rrank,
+                            const int64_t* const* roff, int steps, int warmup, double* out) {
+  try {
+    sf::RunConfig cfg;
+    cfg.nranks = nranks;
+    cfg.timeout_s = 3600.0;
+    std::vector<double> setup_s(static_cast<size_t>(nranks)), step_us(static_cast<size_t>(nranks)),
+        b_us(static_cast<size_t>(nranks)), r_us(static_cast<size_t>(nranks));
+    sf::run_ranks(cfg, [&](sf::Comm& comm) {
+      using clk = std::chrono::steady_clock;
+      const int r = comm.rank();
+      sf::StarForest f(comm);
+      f.set_graph(make_spec(r, nroots, nleaves, local, rrank, roff));
+      comm.barrier();
+      const auto t0 = clk::now();
+      f.setup();
+      setup_s[static_cast<size_t>(r)] = std::chrono::duration<double>(clk::now() - t0).count();
+      std::vector<double> root(static_cast<size_t>(nroots[r])), leaf(static_cast<size_t>(f.leaf_index_bound()));
+      for (size_t i = 0; i < root.size(); ++i) root[i] = 1.0 + static_cast<double>(i % 97) * 1e-3;
+      for (size_t i = 0; i < leaf.size(); ++i) leaf[i] = 0.0;
+      const sf::Unit u = sf::unit_of<double>();
+      for (int w = 0; w < warmup; ++w) {
+        sf::bcast(f, u, root.data(), leaf.data(), sf::ReduceOp::replace);
+        sf::reduce(f, u, leaf.data(), root.data(), sf::ReduceOp::sum);
+      }
+      double tb = 0, tr = 0;
+      comm.barrier();
+      const auto s0 = clk::now();
+      for (int s = 0; s < steps; ++s) {
+        const auto a0 = clk::now();
+        sf::bcast(f, u, root.data(), leaf.data(), sf::ReduceOp::replace);
+        const auto a1 = clk::now();
+        sf::reduce(f, u, leaf.data(), root.data(), sf::ReduceOp::sum);
+        const auto a2 = clk::now();
+        tb += std::chrono::duration<double, std::micro>(a1 - a0).count();
+        tr += std::chrono::duration<double, std::micro>(a2 - a1).count();
+      }
+      const auto s1 = clk::now();
+      comm.barrier();
+      step_us[static_cast<size_t>(r)] = std::chrono::duration<double, std::micro>(s1 - s0).count() / steps;
+      b_us[static_cast<size_t>(r)] = tb / steps;
+      r_us[static_cast<size_t>(r)] = tr / steps;
+    });
+    double ms = 0, mu = 0;
+    for (int r = 0; r < nranks; ++r) {
+      ms = std::max(ms, setup_s[static_cast<size_t>(r)]);
+      mu = std::max(mu, step_us[static_cast<size_t>(r)]);
+    }
+    out[0] = ms;
+    out[1] = mu;
+    out[2] = b_us[0];
+    out[3] = r_us[0];
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,358 @@
+// extern "C" boundary (include/sfgpu.h). Converts C++ exceptions to status
+// codes + a thread-local message, the C rendering of sf::Error.
+#include "../../include/sfgpu.h"
+
+#include <cstring>
+#include <string>
+
+#include "sfg.hpp"
+
+struct sfg_world_s {
+  sfg::World w;
+  sfg_world_s(int n, double t) : w(n, t) {}
+};
+struct sfg_comm_s {
+  std::unique_ptr<sfg::World> own_world;
+  std::unique_ptr<sfg::Comm> c;
+};
+struct sfg_sf_s {};      // alias of sfg::StarForest
+struct sfg_handle_s {};  // alias of sfg::OpHandle
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail_code(const std::exception& e, int code) {
+  g_err = e.what();
+  return code;
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return SFG_OK;
+  } catch (const sfg::TimeoutError& e) {
+    return fail_code(e, SFG_ERR_TIMEOUT);
+  } catch (const sfg::CudaError& e) {
+    return fail_code(e, SFG_ERR_CUDA);
+  } catch (const std::exception& e) {
+    return fail_code(e, SFG_ERR);
+  }
+}
+
+sfg::StarForest* SF(sfg_sf s) {
+  SFG_REQUIRE(s != nullptr, "null star forest");
+  return reinterpret_cast<sfg::StarForest*>(s);
+}
+sfg::OpHandle* H(sfg_handle h) {
+  SFG_REQUIRE(h != nullptr, "null operation handle");
+  return reinterpret_cast<sfg::OpHandle*>(h);
+}
+sfg_handle out_h(std::unique_ptr<sfg::OpHandle> h) {
+  return reinterpret_cast<sfg_handle>(h.release());
+}
+sfg::Unit unit(int kind, int64_t blocklen) {
+  SFG_REQUIRE(kind >= 0 && kind <= 3, "unknown unit kind");
+  return sfg::Unit{static_cast<sfg::Kind>(kind), blocklen};
+}
+sfg::ReduceOp rop(int op) {
+  SFG_REQUIRE(op >= 0 && op <= 8, "unknown reduction");
+  return static_cast<sfg::ReduceOp>(op);
+}
+cudaStream_t st(void* s) { return static_cast<cudaStream_t>(s); }
+
+void fill_pattern(const sfg::Pattern& p, sfg_pattern* o) {
+  o->kind = static_cast<int>(p.kind);
+  o->has_duplicates = p.has_duplicates ? 1 : 0;
+  o->count = p.count;
+  o->start = p.start;
+  o->dx = p.dx;
+  o->dy = p.dy;
+  o->dz = p.dz;
+  o->s1 = p.s1;
+  o->s2 = p.s2;
+  o->bound = p.bound;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sfg_last_error(void) { return g_err.c_str(); }
+int sfg_version(void) { return SFGPU_VERSION; }
+
+void sfg_config_default(sfg_config* cfg) {
+  sfg::CommConfig c;
+  cfg->deterministic = c.deterministic ? 1 : 0;
+  cfg->debug_checksum = c.debug_checksum ? 1 : 0;
+  cfg->force_remote = c.force_remote ? 1 : 0;
+  cfg->dense_discovery_threshold = c.dense_discovery_threshold;
+  cfg->seed = c.seed;
+  cfg->timeout_s = c.timeout_s;
+}
+
+int sfg_world_create(int nranks, double timeout_s, sfg_world* out) {
+  return guard([&] { *out = new sfg_world_s(nranks, timeout_s); });
+}
+int sfg_world_abort(sfg_world w) {
+  return guard([&] { w->w.abort(); });
+}
+int sfg_world_destroy(sfg_world w) {
+  return guard([&] { delete w; });
+}
+
+int sfg_nccl_unique_id(void* out, size_t bytes) {
+  return guard([&] {
+    SFG_REQUIRE(bytes >= sizeof(ncclUniqueId), "unique id buffer too small");
+    ncclUniqueId id;
+    SFG_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+int sfg_comm_create(sfg_world world, int nranks, int rank, int device, const char* backend,
+                    const void* nccl_id, const sfg_config* cfg, sfg_comm* out) {
+  return guard([&] {
+    sfg::CommConfig cc;
+    if (cfg) {
+      cc.deterministic = cfg->deterministic != 0;
+      cc.debug_checksum = cfg->debug_checksum != 0;
+      cc.force_remote = cfg->force_remote != 0;
+      cc.dense_discovery_threshold = cfg->dense_discovery_threshold;
+      cc.seed = cfg->seed;
+      cc.timeout_s = cfg->timeout_s;
+    }
+    cc.backend = backend ? backend : "threads";
+    SFG_REQUIRE(cc.backend == "threads" || cc.backend == "nccl",
+                "unknown transport backend '" + cc.backend + "' (threads | nccl)");
+    auto h = std::make_unique<sfg_comm_s>();
+    h->c = std::make_unique<sfg::Comm>(nranks, rank, device, cc);
+    sfg::Comm& c = *h->c;
+    sfg::World* w = world ? &world->w : nullptr;
+    if (w) SFG_REQUIRE(w->size() == nranks, "world size does not match nranks");
+    if (!w && cc.backend == "threads") {
+      SFG_REQUIRE(nranks == 1, "the threads backend needs an in-process world for nranks > 1");
+      h->own_world = std::make_unique<sfg::World>(1, cc.timeout_s);
+      w = h->own_world.get();
+    }
+    c.world_ = w;
+    if (device >= 0) {
+      SFG_CUDA(cudaSetDevice(device));
+      SFG_CUDA(cudaFree(nullptr));  // create the context
+    }
+    if (cc.backend == "nccl") {
+      SFG_REQUIRE(device >= 0, "the nccl backend needs a device");
+      ncclUniqueId id;
+      if (nccl_id) {
+        std::memcpy(&id, nccl_id, sizeof(id));
+      } else {
+        SFG_REQUIRE(nranks == 1, "nccl backend with nranks > 1 needs a shared unique id");
+        SFG_NCCL(ncclGetUniqueId(&id));
+      }
+      SFG_NCCL(ncclCommInitRank(&c.nccl_, nranks, id, rank));
+    }
+    if (w)
+      c.ctrl_ = sfg::make_threads_ctrl(w, rank);
+    else if (nranks == 1)
+      c.ctrl_ = sfg::make_single_ctrl();
+    else
+      c.ctrl_ = sfg::make_nccl_ctrl(c.nccl_, rank, nranks, device);
+    if (device >= 0) {
+      if (cc.backend == "nccl")
+        c.transport_ = sfg::make_nccl_transport(c.nccl_, rank, device);
+      else
+        c.transport_ = sfg::make_threads_transport(w, rank, device, cc.timeout_s);
+    }
+    *out = h.release();
+  });
+}
+
+int sfg_comm_destroy(sfg_comm c) {
+  return guard([&] { delete c; });
+}
+
+int sfg_comm_rank(sfg_comm c, int* rank, int* size, int* device) {
+  return guard([&] {
+    if (rank) *rank = c->c->rank();
+    if (size) *size = c->c->size();
+    if (device) *device = c->c->device();
+  });
+}
+
+int sfg_sf_create(sfg_comm c, sfg_sf* out) {
+  return guard([&] {
+    SFG_REQUIRE(c != nullptr, "star forest needs a valid communicator");
+    *out = reinterpret_cast<sfg_sf>(new sfg::StarForest(c->c.get()));
+  });
+}
+
+int sfg_sf_destroy(sfg_sf sf) {
+  return guard([&] { delete SF(sf); });
+}
+
+int sfg_sf_set_graph(sfg_sf sf, int64_t nroots, int64_t nleaves, const int64_t* leaf_local,
+                     const int32_t* remote_rank, const int64_t* remote_off) {
+  return guard([&] { SF(sf)->set_graph(nroots, nleaves, leaf_local, remote_rank, remote_off); });
+}
+
+int sfg_sf_setup(sfg_sf sf, int alg) {
+  return guard([&] { SF(sf)->setup(static_cast<sfg::SetupAlg>(alg)); });
+}
+
+int sfg_sf_get_info(sfg_sf sf, sfg_sf_info* o) {
+  return guard([&] {
+    auto* s = SF(sf);
+    o->state = static_cast<int>(s->state());
+    o->nroots = s->nroots();
+    o->nleaves = s->nleaves();
+    o->leaf_index_bound = s->leaf_index_bound();
+    o->contiguous_leaves = s->contiguous_leaves() ? 1 : 0;
+    if (s->state() == sfg::SfState::set_up) {
+      o->self_first = s->has_self_edges() ? 1 : 0;
+      o->n_root_groups = static_cast<int>(s->root_groups().size());
+      o->n_leaf_groups = static_cast<int>(s->leaf_groups().size());
+    } else {
+      o->self_first = 0;
+      o->n_root_groups = 0;
+      o->n_leaf_groups = 0;
+    }
+  });
+}
+
+int sfg_sf_group(sfg_sf sf, int which, int g, int* rank, int64_t* nitems, sfg_pattern* pat) {
+  return guard([&] {
+    const auto& gs = which == 0 ? SF(sf)->root_groups() : SF(sf)->leaf_groups();
+    SFG_REQUIRE(g >= 0 && g < static_cast<int>(gs.size()), "group index out of range");
+    if (rank) *rank = gs[static_cast<size_t>(g)].rank;
+    if (nitems) *nitems = static_cast<int64_t>(gs[static_cast<size_t>(g)].items.size());
+    if (pat) fill_pattern(gs[static_cast<size_t>(g)].pat, pat);
+  });
+}
+
+int sfg_sf_group_items(sfg_sf sf, int which, int g, int64_t* items) {
+  return guard([&] {
+    const auto& gs = which == 0 ? SF(sf)->root_groups() : SF(sf)->leaf_groups();
+    SFG_REQUIRE(g >= 0 && g < static_cast<int>(gs.size()), "group index out of range");
+    const auto& v = gs[static_cast<size_t>(g)].items;
+    if (!v.empty()) std::memcpy(items, v.data(), v.size() * sizeof(int64_t));
+  });
+}
+
+int sfg_sf_compute_degrees(sfg_sf sf, int64_t* out) {
+  return guard([&] {
+    auto d = SF(sf)->compute_degrees();
+    if (!d.empty()) std::memcpy(out, d.data(), d.size() * sizeof(int64_t));
+  });
+}
+
+int sfg_sf_multi_sf(sfg_sf sf, sfg_sf* out) {
+  return guard([&] { *out = reinterpret_cast<sfg_sf>(&SF(sf)->multi_sf()); });
+}
+
+int sfg_sf_graph(sfg_sf sf, int64_t* leaf_index, int32_t* remote_rank, int64_t* remote_off) {
+  return guard([&] {
+    auto* s = SF(sf);
+    for (int64_t o = 0; o < s->nleaves(); ++o) {
+      if (leaf_index) leaf_index[o] = s->leaf_index(o);
+      if (remote_rank) remote_rank[o] = s->remote_rank_of(o);
+      if (remote_off) remote_off[o] = s->remote_off_of(o);
+    }
+  });
+}
+
+int sfg_bcast_begin(sfg_sf sf, int kind, int64_t blocklen, const void* rootdata, void* leafdata,
+                    int op, void* stream, sfg_handle* out) {
+  return guard([&] {
+    *out = out_h(sfg::bcast_begin(*SF(sf), unit(kind, blocklen), rootdata, leafdata, rop(op), st(stream)));
+  });
+}
+int sfg_bcast_end(sfg_handle h) {
+  return guard([&] { sfg::bcast_end(*H(h)); });
+}
+
+int sfg_reduce_begin(sfg_sf sf, int kind, int64_t blocklen, const void* leafdata, void* rootdata,
+                     int op, void* stream, sfg_handle* out) {
+  return guard([&] {
+    *out = out_h(sfg::reduce_begin(*SF(sf), unit(kind, blocklen), leafdata, rootdata, rop(op), st(stream)));
+  });
+}
+int sfg_reduce_end(sfg_handle h) {
+  return guard([&] { sfg::reduce_end(*H(h)); });
+}
+
+int sfg_fetch_and_op_begin(sfg_sf sf, int kind, int64_t blocklen, void* rootdata,
+                           const void* leafdata, void* leafupdate, int op, void* stream,
+                           sfg_handle* out) {
+  return guard([&] {
+    *out = out_h(sfg::fetch_and_op_begin(*SF(sf), unit(kind, blocklen), rootdata, leafdata,
+                                         leafupdate, rop(op), st(stream)));
+  });
+}
+int sfg_fetch_and_op_end(sfg_handle h) {
+  return guard([&] { sfg::fetch_and_op_end(*H(h)); });
+}
+
+int sfg_gather_begin(sfg_sf sf, int kind, int64_t blocklen, const void* leafdata,
+                     void* multirootdata, void* stream, sfg_handle* out) {
+  return guard([&] {
+    *out = out_h(sfg::gather_begin(*SF(sf), unit(kind, blocklen), leafdata, multirootdata, st(stream)));
+  });
+}
+int sfg_gather_end(sfg_handle h) {
+  return guard([&] { sfg::gather_end(*H(h)); });
+}
+
+int sfg_scatter_begin(sfg_sf sf, int kind, int64_t blocklen, const void* multirootdata,
+                      void* leafdata, void* stream, sfg_handle* out) {
+  return guard([&] {
+    *out = out_h(sfg::scatter_begin(*SF(sf), unit(kind, blocklen), multirootdata, leafdata, st(stream)));
+  });
+}
+int sfg_scatter_end(sfg_handle h) {
+  return guard([&] { sfg::scatter_end(*H(h)); });
+}
+
+int sfg_handle_info(sfg_handle h, int* opkind, int* op, int* ended) {
+  return guard([&] {
+    auto* x = H(h);
+    if (opkind) *opkind = static_cast<int>(x->kind);
+    if (op) *op = static_cast<int>(x->op);
+    if (ended) *ended = x->ended ? 1 : 0;
+  });
+}
+
+int sfg_handle_free(sfg_handle h) {
+  return guard([&] {
+    auto* x = reinterpret_cast<sfg::OpHandle*>(h);
+    if (x && x->stg && x->sf) x->sf->release_staging(x->stg, x->stream);
+    delete x;
+  });
+}
+
+int sfg_pattern_analyze(const int64_t* idx, int64_t n, int infer_affine, int64_t ex, int64_t exy,
+                        sfg_pattern* out) {
+  return guard([&] { fill_pattern(sfg::Pattern::analyze(idx, n, infer_affine != 0, ex, exy), out); });
+}
+
+int sfg_counters_get(sfg_counters* o) {
+  return guard([&] {
+    auto& c = sfg::counters();
+    o->pack_copies = c.pack_copies;
+    o->pack_elided = c.pack_elided;
+    o->unpack_copies = c.unpack_copies;
+    o->unpack_elided = c.unpack_elided;
+    o->replace_dup_collisions = c.replace_dup_collisions;
+    o->kernel_launches = c.kernel_launches;
+    o->bytes_sent = c.bytes_sent;
+    o->bytes_recv = c.bytes_recv;
+    o->transport_calls = c.transport_calls;
+  });
+}
+
+int sfg_counters_reset(void) {
+  return guard([&] { sfg::counters().reset(); });
+}
+
+}  // extern "C"

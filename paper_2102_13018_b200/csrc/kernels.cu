@@ -1,0 +1,439 @@
+// sm_100a kernels for the star-forest data path.
+//
+// One launch executes a table of segments (see kernels.hpp). Each CTA owns a
+// contiguous block of kThreads*kItems work items of one segment; every thread
+// first resolves all its indices and issues all its loads (kItems independent
+// loads in flight per thread), then applies the reduction and stores. The
+// index maps are evaluated with 32-bit magic-number division so an Affine3D
+// pattern (a 3-D subblock of a ghosted box) costs a few integer ops per
+// element and no index traffic.
+//
+// Reference semantics (what every segment type must reproduce):
+//   ops:      /root/reference/proj/src/pack.cpp:19-45  (MAX is `if (b > a) a = b`)
+//   pack:     /root/reference/proj/src/pack.cpp:111-121
+//   unpack:   /root/reference/proj/src/pack.cpp:138-173
+//   scatter:  /root/reference/proj/src/pack.cpp:220-256
+//   fetch:    /root/reference/proj/src/ops.cpp:110-158, 521-563
+#include <cstdint>
+#include <cstdio>
+#include <type_traits>
+
+#include "kernels.hpp"
+
+namespace sfg {
+namespace {
+
+enum : int {
+  OP_REPLACE = 0,
+  OP_SUM = 1,
+  OP_PROD = 2,
+  OP_MAX = 3,
+  OP_MIN = 4,
+  OP_LAND = 5,
+  OP_LOR = 6,
+  OP_BAND = 7,
+  OP_BOR = 8
+};
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  return (__umulhi(n, f.m) + n) >> f.s;
+}
+
+__device__ __forceinline__ int64_t pat_index(const DPat& p, int64_t i) {
+  if (p.kind == PAT_CONTIG) return p.start + i;
+  if (p.kind == PAT_INDEXED) return static_cast<int64_t>(__ldg(p.idx + i));
+  const uint32_t ui = static_cast<uint32_t>(i);
+  const uint32_t row = fdiv(ui, p.dx);
+  const uint32_t x = ui - row * p.dx.d;
+  const uint32_t z = fdiv(row, p.dy);
+  const uint32_t y = row - z * p.dy.d;
+  return p.start + static_cast<int64_t>(x) + static_cast<int64_t>(y) * p.s1 +
+         static_cast<int64_t>(z) * p.s2;
+}
+
+template <class T>
+struct Unsigned {
+  using type = T;
+};
+template <>
+struct Unsigned<int32_t> {
+  using type = uint32_t;
+};
+template <>
+struct Unsigned<int64_t> {
+  using type = uint64_t;
+};
+
+// a (op)= b with the reference's exact semantics; integer arithmetic wraps.
+template <class T, int OP>
+__device__ __forceinline__ T apply_op(T a, T b) {
+  if constexpr (OP == OP_REPLACE) {
+    return b;
+  } else if constexpr (OP == OP_SUM) {
+    if constexpr (std::is_same_v<T, double>)
+      return __dadd_rn(a, b);
+    else
+      return static_cast<T>(static_cast<typename Unsigned<T>::type>(a) +
+                            static_cast<typename Unsigned<T>::type>(b));
+  } else if constexpr (OP == OP_PROD) {
+    if constexpr (std::is_same_v<T, double>)
+      return __dmul_rn(a, b);
+    else
+      return static_cast<T>(static_cast<typename Unsigned<T>::type>(a) *
+                            static_cast<typename Unsigned<T>::type>(b));
+  } else if constexpr (OP == OP_MAX) {
+    return (b > a) ? b : a;
+  } else if constexpr (OP == OP_MIN) {
+    return (b < a) ? b : a;
+  } else if constexpr (OP == OP_LAND) {
+    return (a && b) ? T(1) : T(0);
+  } else if constexpr (OP == OP_LOR) {
+    return (a || b) ? T(1) : T(0);
+  } else if constexpr (OP == OP_BAND) {
+    if constexpr (std::is_integral_v<T>) return a & b;
+    return a;
+  } else {
+    if constexpr (std::is_integral_v<T>) return a | b;
+    return a;
+  }
+}
+
+// Atomic read-modify-write returning the previous value. Native atomics where
+// the hardware has them, a CAS loop with the reference comparison otherwise.
+template <class T, int OP>
+__device__ __forceinline__ T atomic_fetch_apply(T* p, T v) {
+  if constexpr (sizeof(T) < 4) {
+    __trap();
+    return v;
+  } else if constexpr (OP == OP_SUM && std::is_same_v<T, double>) {
+    return atomicAdd(p, v);
+  } else if constexpr (OP == OP_SUM && sizeof(T) == 8) {
+    return static_cast<T>(atomicAdd(reinterpret_cast<unsigned long long*>(p),
+                                    static_cast<unsigned long long>(v)));
+  } else if constexpr (OP == OP_SUM && sizeof(T) == 4) {
+    return static_cast<T>(
+        atomicAdd(reinterpret_cast<unsigned int*>(p), static_cast<unsigned int>(v)));
+  } else if constexpr (OP == OP_MAX && std::is_same_v<T, int64_t>) {
+    return static_cast<T>(atomicMax(reinterpret_cast<long long*>(p), static_cast<long long>(v)));
+  } else if constexpr (OP == OP_MIN && std::is_same_v<T, int64_t>) {
+    return static_cast<T>(atomicMin(reinterpret_cast<long long*>(p), static_cast<long long>(v)));
+  } else if constexpr (OP == OP_MAX && std::is_same_v<T, int32_t>) {
+    return atomicMax(p, v);
+  } else if constexpr (OP == OP_MIN && std::is_same_v<T, int32_t>) {
+    return atomicMin(p, v);
+  } else if constexpr (OP == OP_BAND && std::is_integral_v<T> && sizeof(T) == 8) {
+    return static_cast<T>(atomicAnd(reinterpret_cast<unsigned long long*>(p),
+                                    static_cast<unsigned long long>(v)));
+  } else if constexpr (OP == OP_BOR && std::is_integral_v<T> && sizeof(T) == 8) {
+    return static_cast<T>(atomicOr(reinterpret_cast<unsigned long long*>(p),
+                                   static_cast<unsigned long long>(v)));
+  } else if constexpr (OP == OP_BAND && std::is_integral_v<T> && sizeof(T) == 4) {
+    return static_cast<T>(
+        atomicAnd(reinterpret_cast<unsigned int*>(p), static_cast<unsigned int>(v)));
+  } else if constexpr (OP == OP_BOR && std::is_integral_v<T> && sizeof(T) == 4) {
+    return static_cast<T>(
+        atomicOr(reinterpret_cast<unsigned int*>(p), static_cast<unsigned int>(v)));
+  } else if constexpr (sizeof(T) == 8) {
+    auto* a = reinterpret_cast<unsigned long long*>(p);
+    unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(a);
+    unsigned long long assumed;
+    T cur;
+    do {
+      assumed = old;
+      cur = *reinterpret_cast<T*>(&assumed);
+      T nv = apply_op<T, OP>(cur, v);
+      unsigned long long nb = *reinterpret_cast<unsigned long long*>(&nv);
+      if (nb == assumed) return cur;
+      old = atomicCAS(a, assumed, nb);
+    } while (old != assumed);
+    return cur;
+  } else {
+    auto* a = reinterpret_cast<unsigned int*>(p);
+    unsigned int old = *reinterpret_cast<volatile unsigned int*>(a);
+    unsigned int assumed;
+    T cur;
+    do {
+      assumed = old;
+      cur = *reinterpret_cast<T*>(&assumed);
+      T nv = apply_op<T, OP>(cur, v);
+      unsigned int nb = *reinterpret_cast<unsigned int*>(&nv);
+      if (nb == assumed) return cur;
+      old = atomicCAS(a, assumed, nb);
+    } while (old != assumed);
+    return cur;
+  }
+}
+
+struct ItemMap {
+  int64_t bl;
+  bool small;
+  FastDiv f;
+  __device__ __forceinline__ void split(int64_t e, int64_t& i, int64_t& k) const {
+    if (bl == 1) {
+      i = e;
+      k = 0;
+    } else if (small) {
+      i = fdiv(static_cast<uint32_t>(e), f);
+      k = e - i * bl;
+    } else {
+      i = e / bl;
+      k = e - i * bl;
+    }
+  }
+};
+
+// dst[dpat(i)] (op)= src[spat(i)] over this CTA's items.
+template <class T, int OP, bool ATOMIC>
+__device__ __forceinline__ void run_pair(const DSeg& s, const LaunchParams& P, int64_t blk) {
+  const T* __restrict__ src = static_cast<const T*>(P.bufs[s.src_buf]);
+  T* dst = static_cast<T*>(P.bufs[s.dst_buf]);
+  const int64_t total = s.n * P.bl;
+  const ItemMap im{P.bl, total < (int64_t(1) << 31), P.bldiv};
+  const int64_t base = blk * (kThreads * kItems) + threadIdx.x;
+  T v[kItems];
+  T d[kItems];
+  int64_t di[kItems];
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    const int64_t e = base + static_cast<int64_t>(u) * kThreads;
+    di[u] = -1;
+    if (e < total) {
+      int64_t i, k;
+      im.split(e, i, k);
+      const int64_t si = pat_index(s.src, i) * P.bl + k;
+      di[u] = pat_index(s.dst, i) * P.bl + k;
+      v[u] = src[si];
+      if constexpr (OP != OP_REPLACE && !ATOMIC) d[u] = dst[di[u]];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    if (di[u] < 0) continue;
+    if constexpr (OP == OP_REPLACE) {
+      dst[di[u]] = v[u];
+    } else if constexpr (ATOMIC) {
+      (void)atomic_fetch_apply<T, OP>(dst + di[u], v[u]);
+    } else {
+      dst[di[u]] = apply_op<T, OP>(d[u], v[u]);
+    }
+  }
+}
+
+// Root-sorted fold in the reference order (self leaves ascending, then remote
+// groups ascending rank, each in ascending leaf order). Sequential per root,
+// so floating-point results are bit-identical to the CPU reference.
+template <class T, int OP>
+__device__ __forceinline__ void run_csr(const DSeg& s, const LaunchParams& P, int64_t blk,
+                                        bool fetch) {
+  T* root = static_cast<T*>(P.bufs[s.dst_buf]);
+  const T* leaf = static_cast<const T*>(P.bufs[s.src_buf]);
+  T* stage = static_cast<T*>(P.bufs[s.stage_buf]);
+  T* aux = static_cast<T*>(P.bufs[s.aux_buf]);
+  const int64_t bl = P.bl;
+  const int64_t total = s.n * bl;
+  const ItemMap im{bl, total < (int64_t(1) << 31), P.bldiv};
+  const int64_t base = blk * (kThreads * kItems) + threadIdx.x;
+#pragma unroll 1
+  for (int u = 0; u < kItems; ++u) {
+    const int64_t e = base + static_cast<int64_t>(u) * kThreads;
+    if (e >= total) break;
+    int64_t r, k;
+    im.split(e, r, k);
+    const int32_t lo = __ldg(s.csr_lo + r);
+    const int32_t hi = __ldg(s.csr_hi + r);
+    if (lo >= hi) continue;
+    const int64_t ro = static_cast<int64_t>(__ldg(s.csr_roots + r)) * bl + k;
+    T acc = root[ro];
+    int32_t j = lo;
+    // Batches of 4: issue the index and value loads before the dependent fold.
+    for (; j + 4 <= hi; j += 4) {
+      int32_t en[4];
+      T c[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) en[q] = __ldg(s.csr_ent + j + q);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        c[q] = en[q] >= 0 ? leaf[static_cast<int64_t>(en[q]) * bl + k]
+                          : stage[static_cast<int64_t>(-en[q] - 1) * bl + k];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (fetch) {
+          if (en[q] >= 0)
+            aux[static_cast<int64_t>(en[q]) * bl + k] = acc;
+          else
+            stage[static_cast<int64_t>(-en[q] - 1) * bl + k] = acc;
+        }
+        acc = apply_op<T, OP>(acc, c[q]);
+      }
+    }
+    for (; j < hi; ++j) {
+      const int32_t en = __ldg(s.csr_ent + j);
+      const T c = en >= 0 ? leaf[static_cast<int64_t>(en) * bl + k]
+                          : stage[static_cast<int64_t>(-en - 1) * bl + k];
+      if (fetch) {
+        if (en >= 0)
+          aux[static_cast<int64_t>(en) * bl + k] = acc;
+        else
+          stage[static_cast<int64_t>(-en - 1) * bl + k] = acc;
+      }
+      acc = apply_op<T, OP>(acc, c);
+    }
+    root[ro] = acc;
+  }
+}
+
+// Free-order fetch-and-op: fetched = atomic(root[dpat(i)] op= src[spat(i)]),
+// written to aux[spat(i)] (leafupdate for self edges, the reply slot in place
+// for remote contributions).
+template <class T, int OP>
+__device__ __forceinline__ void run_atomic_fetch(const DSeg& s, const LaunchParams& P,
+                                                 int64_t blk) {
+  const T* src = static_cast<const T*>(P.bufs[s.src_buf]);
+  T* root = static_cast<T*>(P.bufs[s.dst_buf]);
+  T* aux = static_cast<T*>(P.bufs[s.aux_buf]);
+  const int64_t total = s.n * P.bl;
+  const ItemMap im{P.bl, total < (int64_t(1) << 31), P.bldiv};
+  const int64_t base = blk * (kThreads * kItems) + threadIdx.x;
+  T v[kItems];
+  int64_t si[kItems], di[kItems];
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    const int64_t e = base + static_cast<int64_t>(u) * kThreads;
+    di[u] = -1;
+    if (e < total) {
+      int64_t i, k;
+      im.split(e, i, k);
+      si[u] = pat_index(s.src, i) * P.bl + k;
+      di[u] = pat_index(s.dst, i) * P.bl + k;
+      v[u] = src[si[u]];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    if (di[u] < 0) continue;
+    aux[si[u]] = atomic_fetch_apply<T, OP>(root + di[u], v[u]);
+  }
+}
+
+template <class T, int OP>
+__global__ void __launch_bounds__(kThreads) segments_kernel(const __grid_constant__ LaunchParams P) {
+  const int64_t b = blockIdx.x;
+  int s = 0;
+  while (s + 1 < P.nseg && b >= P.block_start[s + 1]) ++s;
+  const DSeg& seg = P.seg[s];
+  const int64_t blk = b - P.block_start[s];
+  switch (seg.type) {
+    case SEG_PAIR:
+      if (seg.replace)
+        run_pair<T, OP_REPLACE, false>(seg, P, blk);
+      else
+        run_pair<T, OP, false>(seg, P, blk);
+      break;
+    case SEG_PAIR_ATOMIC:
+      if constexpr (OP != OP_REPLACE && sizeof(T) >= 4) run_pair<T, OP, true>(seg, P, blk);
+      break;
+    case SEG_CSR_FOLD:
+      if constexpr (OP != OP_REPLACE) run_csr<T, OP>(seg, P, blk, false);
+      break;
+    case SEG_CSR_FETCH:
+      if constexpr (OP != OP_REPLACE) run_csr<T, OP>(seg, P, blk, true);
+      break;
+    case SEG_ATOMIC_FETCH:
+      if constexpr (OP != OP_REPLACE && sizeof(T) >= 4) run_atomic_fetch<T, OP>(seg, P, blk);
+      break;
+    default:
+      break;
+  }
+}
+
+template <class T, int OP>
+void launch_t(const LaunchParams& p, int64_t blocks, cudaStream_t st) {
+  segments_kernel<T, OP><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
+}
+
+template <class T>
+bool launch_int_ops(const LaunchParams& p, int op, int64_t blocks, cudaStream_t st) {
+  switch (op) {
+    case OP_REPLACE: launch_t<T, OP_REPLACE>(p, blocks, st); return true;
+    case OP_SUM: launch_t<T, OP_SUM>(p, blocks, st); return true;
+    case OP_PROD: launch_t<T, OP_PROD>(p, blocks, st); return true;
+    case OP_MAX: launch_t<T, OP_MAX>(p, blocks, st); return true;
+    case OP_MIN: launch_t<T, OP_MIN>(p, blocks, st); return true;
+    case OP_LAND: launch_t<T, OP_LAND>(p, blocks, st); return true;
+    case OP_LOR: launch_t<T, OP_LOR>(p, blocks, st); return true;
+    case OP_BAND: launch_t<T, OP_BAND>(p, blocks, st); return true;
+    case OP_BOR: launch_t<T, OP_BOR>(p, blocks, st); return true;
+  }
+  return false;
+}
+
+bool launch_f64_ops(const LaunchParams& p, int op, int64_t blocks, cudaStream_t st) {
+  switch (op) {
+    case OP_REPLACE: launch_t<double, OP_REPLACE>(p, blocks, st); return true;
+    case OP_SUM: launch_t<double, OP_SUM>(p, blocks, st); return true;
+    case OP_PROD: launch_t<double, OP_PROD>(p, blocks, st); return true;
+    case OP_MAX: launch_t<double, OP_MAX>(p, blocks, st); return true;
+    case OP_MIN: launch_t<double, OP_MIN>(p, blocks, st); return true;
+  }
+  return false;
+}
+
+__global__ void digest_kernel(const unsigned char* p, size_t bytes, unsigned long long* out) {
+  const size_t nwords = bytes / 8;
+  unsigned long long acc = 0;
+  const auto* w = reinterpret_cast<const unsigned long long*>(p);
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < nwords;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    unsigned long long z = w[i] ^ (static_cast<unsigned long long>(i) * 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    acc += z ^ (z >> 31);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (size_t i = nwords * 8; i < bytes; ++i) acc += (static_cast<unsigned long long>(p[i]) + 1) * (i + 7);
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
+}  // namespace
+
+int launch_segments(LaunchParams& p, ElemType t, int op, cudaStream_t stream) {
+  int64_t blocks = 0;
+  int n = 0;
+  for (int s = 0; s < p.nseg; ++s) {
+    const int64_t items = p.seg[s].n * p.bl;
+    if (items <= 0) continue;
+    p.seg[n] = p.seg[s];
+    p.block_start[n] = blocks;
+    blocks += (items + kThreads * kItems - 1) / (kThreads * kItems);
+    ++n;
+  }
+  p.nseg = n;
+  p.block_start[n] = blocks;
+  if (blocks == 0) return 0;
+  p.bldiv = make_fastdiv(static_cast<uint32_t>(p.bl > 0x7fffffff ? 1 : p.bl));
+  bool ok = false;
+  switch (t) {
+    case ElemType::u8: ok = op == OP_REPLACE && (launch_t<uint8_t, OP_REPLACE>(p, blocks, stream), true); break;
+    case ElemType::u16: ok = op == OP_REPLACE && (launch_t<uint16_t, OP_REPLACE>(p, blocks, stream), true); break;
+    case ElemType::u32: ok = op == OP_REPLACE && (launch_t<uint32_t, OP_REPLACE>(p, blocks, stream), true); break;
+    case ElemType::u64: ok = op == OP_REPLACE && (launch_t<uint64_t, OP_REPLACE>(p, blocks, stream), true); break;
+    case ElemType::i32: ok = launch_int_ops<int32_t>(p, op, blocks, stream); break;
+    case ElemType::i64: ok = launch_int_ops<int64_t>(p, op, blocks, stream); break;
+    case ElemType::f64: ok = launch_f64_ops(p, op, blocks, stream); break;
+  }
+  if (!ok) return -1;
+  return 1;
+}
+
+void launch_digest(const void* p, size_t bytes, unsigned long long* out_dev, cudaStream_t s) {
+  cudaMemsetAsync(out_dev, 0, sizeof(unsigned long long), s);
+  if (bytes == 0) return;
+  size_t words = bytes / 8;
+  int blocks = static_cast<int>(words / (256 * 8) + 1);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  digest_kernel<<<blocks, 256, 0, s>>>(static_cast<const unsigned char*>(p), bytes, out_dev);
+}
+
+}  // namespace sfg

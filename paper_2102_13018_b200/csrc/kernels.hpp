@@ -1,0 +1,115 @@
+// Device-side plan descriptors and the launch interface shared by the host
+// engine (ops.cpp) and the sm_100a kernels (kernels.cu).
+//
+// Every data movement the star-forest engine performs is a list of
+// "segments" executed by ONE kernel launch:
+//   SEG_PAIR         dst[dpat(i)] (op)= src[spat(i)]  (pack, unpack, local
+//                    scatter; the reference's pack/unpack/scatter loops,
+//                    /root/reference/proj/src/pack.cpp:111-256)
+//   SEG_PAIR_ATOMIC  same with per-element atomics (free-order mode)
+//   SEG_CSR_FOLD     root-sorted fold: root[r] = fold(root[r], contributions
+//                    in the reference's deterministic order) — bit-exact with
+//                    /root/reference/proj/src/ops.cpp:364,367-376
+//   SEG_CSR_FETCH    serialized fetch-and-op over the same CSR
+//                    (/root/reference/proj/src/ops.cpp:521-563)
+//   SEG_ATOMIC_FETCH free-order fetch-and-op with atomics
+// Patterns are Contiguous, Affine3D (start + x + y*s1 + z*s2) or Indexed.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sfg {
+
+enum PatKind : uint32_t { PAT_CONTIG = 0, PAT_AFFINE = 1, PAT_INDEXED = 2 };
+
+// Unsigned 32-bit division by a run-time constant (round-up multiplier).
+// Valid for numerators < 2^31, which holds for every per-rank position.
+struct FastDiv {
+  uint32_t d = 1, m = 0, s = 0;
+};
+
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d == 0 ? 1 : d;
+  uint32_t l = 0;
+  while ((uint64_t(1) << l) < f.d) ++l;
+  f.s = l;
+  // m = floor(2^32 * (2^l - d) / d) + 1
+  f.m = static_cast<uint32_t>(((uint64_t(1) << 32) * ((uint64_t(1) << l) - f.d)) / f.d + 1);
+  return f;
+}
+
+struct DPat {
+  int64_t start = 0;  // contiguous / affine base (vertex index)
+  int64_t s1 = 0;     // affine row stride (vertices)
+  int64_t s2 = 0;     // affine plane stride (vertices)
+  const int32_t* idx = nullptr;  // indexed
+  uint32_t kind = PAT_CONTIG;
+  uint32_t pad = 0;
+  FastDiv dx;  // affine row length
+  FastDiv dy;  // affine rows per plane
+};
+
+enum SegType : int32_t {
+  SEG_PAIR = 0,
+  SEG_PAIR_ATOMIC = 1,
+  SEG_CSR_FOLD = 2,
+  SEG_CSR_FETCH = 3,
+  SEG_ATOMIC_FETCH = 4,
+};
+
+// Buffer slots a segment can address; filled per call.
+enum BufId : int32_t {
+  BUF_ROOT = 0,        // user rootdata (or multiroot data)
+  BUF_LEAF = 1,        // user leafdata
+  BUF_LEAF_STAGE = 2,  // leaf-side staging (remote root groups, wire order)
+  BUF_ROOT_STAGE = 3,  // root-side staging (remote leaf groups, wire order)
+  BUF_LEAFUPDATE = 4,  // fetch-and-op leafupdate
+  BUF_LEAF_REPLY = 5,  // fetch-and-op reply staging on the leaf side
+  BUF_SRC_RO = 6,      // read-only source alias (leafdata for reduce/fetch)
+  BUF_COUNT = 8
+};
+
+struct DSeg {
+  DPat src;
+  DPat dst;
+  int64_t n = 0;  // positions (pair) or CSR roots (csr)
+  int32_t type = SEG_PAIR;
+  int32_t replace = 0;  // 1: this segment moves data verbatim (pack)
+  int32_t src_buf = 0;
+  int32_t dst_buf = 0;
+  int32_t aux_buf = 0;   // fetch: where fetched values go (same pattern as src)
+  int32_t stage_buf = 0; // csr: buffer of remote entries (entry < 0)
+  // CSR over distinct roots: roots[r], contributions ent[lo[r] .. hi[r])
+  // entry >= 0: self leaf index into src_buf; entry < 0: staging position -e-1
+  const int32_t* csr_roots = nullptr;
+  const int32_t* csr_lo = nullptr;
+  const int32_t* csr_hi = nullptr;
+  const int32_t* csr_ent = nullptr;
+};
+
+constexpr int kMaxSegs = 12;
+constexpr int kThreads = 256;
+constexpr int kItems = 8;  // work items per thread per block
+
+struct LaunchParams {
+  DSeg seg[kMaxSegs];
+  int64_t block_start[kMaxSegs + 1];  // prefix of blocks per segment
+  void* bufs[BUF_COUNT];
+  int64_t bl = 1;  // elements per vertex
+  FastDiv bldiv;
+  int nseg = 0;
+  int vec_ok = 0;  // reserved
+};
+
+// Element type the kernel instantiates for.
+enum class ElemType : int32_t { u8, u16, u32, u64, i32, i64, f64 };
+
+// Returns number of kernel launches issued (0 or 1 per call).
+int launch_segments(LaunchParams& p, ElemType t, int op, cudaStream_t stream);
+
+// Order-independent 64-bit digest of a device buffer (debug checksum).
+void launch_digest(const void* p, size_t bytes, unsigned long long* out_dev, cudaStream_t s);
+
+}  // namespace sfg

@@ -1,0 +1,522 @@
+// Split-phase operations: Bcast, Reduce, FetchAndOp, Gather, Scatter.
+//
+// Reference engines: /root/reference/proj/src/ops.cpp
+//   root->leaf two-sided  :276-324   (bcast, scatter)
+//   leaf->root two-sided  :326-376   (reduce, gather)
+//   fetch-and-op          :481-570
+//   public begin/end      :697-876
+// Per Begin: ONE fused kernel launch packs every remote group whose pattern
+// is not contiguous and performs the local (self-edge) scatter, then ONE
+// grouped transport call posts all sends and receives on the caller's
+// stream. Per End: the transport's receives are ordered before ONE unpack
+// launch. Contiguous patterns are zero-copy on the send side, and on the
+// receive side when op == REPLACE (ops.cpp:289-291,339-341). Nothing
+// synchronises the host with the GPU (§V "stream-aware, sync-free").
+//
+// Fold order. Where a reduction can hit the same root more than once, the
+// deterministic mode (CommConfig::deterministic, the reference default) folds
+// through a root-sorted CSR in exactly the reference order — initial value,
+// self edges by ascending leaf index, then remote ranks ascending, each in
+// ascending leaf index (ops.cpp:364,372-376; oracle.cpp:84-90) — so
+// floating-point results are bit-identical to the CPU reference. The
+// free-order mode uses atomics (pack.cpp:47-58 "atomics" mode).
+#include <cstring>
+
+#include "sfg.hpp"
+
+namespace sfg {
+namespace {
+
+constexpr int kOpReplace = 0;
+
+DPat contig(int64_t start) {
+  DPat p;
+  p.kind = PAT_CONTIG;
+  p.start = start;
+  return p;
+}
+
+DSeg pair_seg(const DPat& src, int sbuf, const DPat& dst, int dbuf, int64_t n, bool replace,
+              bool atomic = false) {
+  DSeg s;
+  s.src = src;
+  s.dst = dst;
+  s.src_buf = sbuf;
+  s.dst_buf = dbuf;
+  s.n = n;
+  s.replace = replace ? 1 : 0;
+  s.type = atomic ? SEG_PAIR_ATOMIC : SEG_PAIR;
+  return s;
+}
+
+enum class CsrRange { self_only, remote_only, all };
+
+DSeg csr_seg(const DevPlan& d, CsrRange range, int32_t type) {
+  DSeg s;
+  s.type = type;
+  s.n = d.csr_n;
+  s.src_buf = BUF_SRC_RO;
+  s.dst_buf = BUF_ROOT;
+  s.aux_buf = BUF_LEAFUPDATE;
+  s.stage_buf = BUF_ROOT_STAGE;
+  s.csr_roots = d.csr_roots;
+  s.csr_ent = d.csr_ent;
+  switch (range) {
+    case CsrRange::self_only:
+      s.csr_lo = d.csr_off;
+      s.csr_hi = d.csr_split;
+      break;
+    case CsrRange::remote_only:
+      s.csr_lo = d.csr_split;
+      s.csr_hi = d.csr_off + 1;
+      break;
+    case CsrRange::all:
+      s.csr_lo = d.csr_off;
+      s.csr_hi = d.csr_off + 1;
+      break;
+  }
+  return s;
+}
+
+// Accumulates the segments of one launch and picks the element type.
+struct Launch {
+  LaunchParams p{};
+  bool any_op = false;
+
+  void add(const DSeg& s) {
+    if (s.n <= 0) return;
+    SFG_REQUIRE(p.nseg < kMaxSegs, "too many segments in one launch");
+    p.seg[p.nseg++] = s;
+    if (!s.replace) any_op = true;
+  }
+
+  void run(const Unit& u, ReduceOp op, cudaStream_t st) {
+    if (p.nseg == 0) return;
+    ElemType t;
+    int kop = static_cast<int>(op);
+    if (!any_op) {
+      // Verbatim move: widest word that divides the vertex size and the
+      // alignment of every buffer involved.
+      uintptr_t align = u.bytes();
+      for (int b = 0; b < BUF_COUNT; ++b)
+        if (p.bufs[b]) align |= reinterpret_cast<uintptr_t>(p.bufs[b]);
+      const size_t ub = u.bytes();
+      if ((align & 7) == 0) {
+        t = ElemType::u64;
+        p.bl = static_cast<int64_t>(ub / 8);
+      } else if ((align & 3) == 0) {
+        t = ElemType::u32;
+        p.bl = static_cast<int64_t>(ub / 4);
+      } else if ((align & 1) == 0) {
+        t = ElemType::u16;
+        p.bl = static_cast<int64_t>(ub / 2);
+      } else {
+        t = ElemType::u8;
+        p.bl = static_cast<int64_t>(ub);
+      }
+      kop = kOpReplace;
+    } else {
+      switch (u.kind) {
+        case Kind::int32: t = ElemType::i32; break;
+        case Kind::int64: t = ElemType::i64; break;
+        case Kind::float64: t = ElemType::f64; break;
+        default: fail("reduction requires a non-opaque unit kind");
+      }
+      p.bl = u.blocklen;
+    }
+    const int launched = launch_segments(p, t, kop, st);
+    SFG_REQUIRE(launched >= 0, "no kernel instantiation for this unit/op combination");
+    SFG_CUDA(cudaGetLastError());
+    counters().kernel_launches += static_cast<uint64_t>(launched);
+  }
+};
+
+void set_bufs(Launch& L, const OpHandle& h, void* root, void* leaf, const void* src_ro) {
+  L.p.bufs[BUF_ROOT] = root;
+  L.p.bufs[BUF_LEAF] = leaf;
+  L.p.bufs[BUF_SRC_RO] = const_cast<void*>(src_ro);
+  if (h.stg) {
+    L.p.bufs[BUF_LEAF_STAGE] = h.stg->leaf_stage;
+    L.p.bufs[BUF_ROOT_STAGE] = h.stg->root_stage;
+    L.p.bufs[BUF_LEAF_REPLY] = h.stg->leaf_reply;
+  }
+  L.p.bufs[BUF_LEAFUPDATE] = h.leafupdate;
+}
+
+uint64_t data_tag(uint64_t opid) { return opid * 2; }
+uint64_t reply_tag(uint64_t opid) { return opid * 2 + 1; }
+
+void* at(void* base, int64_t vertex, size_t ub) {
+  return static_cast<char*>(base) + static_cast<size_t>(vertex) * ub;
+}
+const void* at(const void* base, int64_t vertex, size_t ub) {
+  return static_cast<const char*>(base) + static_cast<size_t>(vertex) * ub;
+}
+
+unsigned long long digest(OpHandle& h, const void* p, size_t bytes) {
+  launch_digest(p, bytes, h.stg->digest, h.stream);
+  unsigned long long v = 0;
+  SFG_CUDA(cudaMemcpyAsync(&v, h.stg->digest, sizeof(v), cudaMemcpyDeviceToHost, h.stream));
+  SFG_CUDA(cudaStreamSynchronize(h.stream));
+  return v;
+}
+
+void begin_common(OpHandle& h, const void* ck_ptr, size_t ck_bytes) {
+  StarForest& sf = *h.sf;
+  sf.comm().bind_device();
+  h.opid = sf.comm().next_op_seq();
+  (void)sf.dev();
+  h.stg = sf.acquire_staging(h.unit.bytes(), h.stream);
+  if (sf.comm().config().debug_checksum && ck_ptr != nullptr && ck_bytes > 0) {
+    h.ck_ptr = ck_ptr;
+    h.ck_bytes = ck_bytes;
+    h.ck_value = digest(h, ck_ptr, ck_bytes);
+  }
+}
+
+void end_common(OpHandle& h) {
+  if (h.ck_ptr != nullptr) {
+    const unsigned long long v = digest(h, h.ck_ptr, h.ck_bytes);
+    if (v != h.ck_value) {
+      h.sf->release_staging(h.stg, h.stream);
+      h.stg = nullptr;
+      fail("buffer mutated between begin and end of a split-phase operation");
+    }
+  }
+  if (h.stg) h.sf->release_staging(h.stg, h.stream);
+  h.stg = nullptr;
+}
+
+// ---------------------------------------------------------- root -> leaf
+void begin_root_to_leaf(OpHandle& h) {
+  StarForest& sf = *h.sf;
+  DevPlan& d = sf.dev();
+  const size_t ub = h.unit.bytes();
+  const bool replace = h.op == ReduceOp::replace;
+  Launch L;
+  set_bufs(L, h, const_cast<void*>(h.src), h.dst, h.src);
+
+  std::vector<XferOp> sends;
+  for (const auto& g : d.lg) {
+    if (g.contiguous) {
+      sends.push_back({g.rank, const_cast<void*>(at(h.src, g.contig_start, ub)), static_cast<size_t>(g.n) * ub});
+      counters().pack_elided++;
+    } else {
+      L.add(pair_seg(g.pat, BUF_ROOT, contig(g.stage_off), BUF_ROOT_STAGE, g.n, true));
+      sends.push_back({g.rank, at(h.stg->root_stage, g.stage_off, ub), static_cast<size_t>(g.n) * ub});
+      counters().pack_copies++;
+    }
+  }
+  if (d.has_self) L.add(pair_seg(d.self_root, BUF_ROOT, d.self_leaf, BUF_LEAF, d.n_self, replace));
+
+  h.recvs.clear();
+  h.zero_copy_recv.clear();
+  for (const auto& g : d.rg) {
+    const bool zc = g.contiguous && replace;
+    h.zero_copy_recv.push_back(zc ? 1 : 0);
+    void* ptr = zc ? at(h.dst, g.contig_start, ub) : at(h.stg->leaf_stage, g.stage_off, ub);
+    h.recvs.push_back({g.rank, ptr, static_cast<size_t>(g.n) * ub});
+    if (zc) counters().unpack_elided++;
+  }
+  L.run(h.unit, h.op, h.stream);
+  if (!sends.empty() || !h.recvs.empty()) {
+    sf.comm().transport().start(data_tag(h.opid), sends, h.recvs, h.stream);
+    counters().transport_calls++;
+  }
+}
+
+void end_root_to_leaf(OpHandle& h) {
+  StarForest& sf = *h.sf;
+  DevPlan& d = sf.dev();
+  const bool replace = h.op == ReduceOp::replace;
+  if (!h.recvs.empty()) sf.comm().transport().finish(data_tag(h.opid), h.recvs, h.stream);
+  Launch L;
+  set_bufs(L, h, const_cast<void*>(h.src), h.dst, h.src);
+  for (size_t k = 0; k < d.rg.size(); ++k) {
+    if (h.zero_copy_recv[k]) continue;
+    const auto& g = d.rg[k];
+    L.add(pair_seg(contig(g.stage_off), BUF_LEAF_STAGE, g.pat, BUF_LEAF, g.n, replace));
+    counters().unpack_copies++;
+  }
+  L.run(h.unit, h.op, h.stream);
+}
+
+// ---------------------------------------------------------- leaf -> root
+void begin_leaf_to_root(OpHandle& h) {
+  StarForest& sf = *h.sf;
+  DevPlan& d = sf.dev();
+  const size_t ub = h.unit.bytes();
+  const bool replace = h.op == ReduceOp::replace;
+  const bool det = sf.comm().config().deterministic;
+  Launch L;
+  set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
+
+  std::vector<XferOp> sends;
+  for (const auto& g : d.rg) {
+    if (g.contiguous) {
+      sends.push_back({g.rank, const_cast<void*>(at(h.src, g.contig_start, ub)), static_cast<size_t>(g.n) * ub});
+      counters().pack_elided++;
+    } else {
+      L.add(pair_seg(g.pat, BUF_LEAF, contig(g.stage_off), BUF_LEAF_STAGE, g.n, true));
+      sends.push_back({g.rank, at(h.stg->leaf_stage, g.stage_off, ub), static_cast<size_t>(g.n) * ub});
+      counters().pack_copies++;
+    }
+  }
+  if (d.has_self) {
+    if (replace && d.self_root_dups) counters().replace_dup_collisions++;
+    if (replace || !d.self_root_dups) {
+      L.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, replace));
+    } else if (det) {
+      sf.ensure_csr();
+      L.add(csr_seg(d, CsrRange::self_only, SEG_CSR_FOLD));
+    } else {
+      L.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, false, true));
+    }
+  }
+
+  h.recvs.clear();
+  h.zero_copy_recv.clear();
+  for (const auto& g : d.lg) {
+    const bool zc = g.contiguous && replace;
+    h.zero_copy_recv.push_back(zc ? 1 : 0);
+    void* ptr = zc ? at(h.dst, g.contig_start, ub) : at(h.stg->root_stage, g.stage_off, ub);
+    h.recvs.push_back({g.rank, ptr, static_cast<size_t>(g.n) * ub});
+    if (zc) counters().unpack_elided++;
+  }
+  L.run(h.unit, h.op, h.stream);
+  if (!sends.empty() || !h.recvs.empty()) {
+    sf.comm().transport().start(data_tag(h.opid), sends, h.recvs, h.stream);
+    counters().transport_calls++;
+  }
+}
+
+void end_leaf_to_root(OpHandle& h) {
+  StarForest& sf = *h.sf;
+  DevPlan& d = sf.dev();
+  const bool replace = h.op == ReduceOp::replace;
+  const bool det = sf.comm().config().deterministic;
+  if (!h.recvs.empty()) sf.comm().transport().finish(data_tag(h.opid), h.recvs, h.stream);
+  Launch L;
+  set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
+  if (!d.lg.empty()) {
+    if (replace || !d.remote_root_dups) {
+      if (replace && d.remote_root_dups) counters().replace_dup_collisions++;
+      for (size_t k = 0; k < d.lg.size(); ++k) {
+        if (h.zero_copy_recv[k]) continue;
+        const auto& g = d.lg[k];
+        L.add(pair_seg(contig(g.stage_off), BUF_ROOT_STAGE, g.pat, BUF_ROOT, g.n, replace));
+        counters().unpack_copies++;
+      }
+    } else if (det) {
+      // Ascending-rank fold of every remote contribution (ops.cpp:372-376).
+      sf.ensure_csr();
+      L.add(csr_seg(d, CsrRange::remote_only, SEG_CSR_FOLD));
+      counters().unpack_copies += d.lg.size();
+    } else {
+      for (const auto& g : d.lg) {
+        L.add(pair_seg(contig(g.stage_off), BUF_ROOT_STAGE, g.pat, BUF_ROOT, g.n, false, true));
+        counters().unpack_copies++;
+      }
+    }
+  }
+  L.run(h.unit, h.op, h.stream);
+}
+
+// ---------------------------------------------------------- fetch-and-op
+void begin_fetch(OpHandle& h) {
+  StarForest& sf = *h.sf;
+  DevPlan& d = sf.dev();
+  const size_t ub = h.unit.bytes();
+  Launch L;
+  set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
+  std::vector<XferOp> sends;
+  for (const auto& g : d.rg) {
+    if (g.contiguous) {
+      sends.push_back({g.rank, const_cast<void*>(at(h.src, g.contig_start, ub)), static_cast<size_t>(g.n) * ub});
+      counters().pack_elided++;
+    } else {
+      L.add(pair_seg(g.pat, BUF_LEAF, contig(g.stage_off), BUF_LEAF_STAGE, g.n, true));
+      sends.push_back({g.rank, at(h.stg->leaf_stage, g.stage_off, ub), static_cast<size_t>(g.n) * ub});
+      counters().pack_copies++;
+    }
+  }
+  h.recvs.clear();
+  for (const auto& g : d.lg)
+    h.recvs.push_back({g.rank, at(h.stg->root_stage, g.stage_off, ub), static_cast<size_t>(g.n) * ub});
+  L.run(h.unit, ReduceOp::replace, h.stream);
+  if (!sends.empty() || !h.recvs.empty()) {
+    sf.comm().transport().start(data_tag(h.opid), sends, h.recvs, h.stream);
+    counters().transport_calls++;
+  }
+}
+
+void end_fetch(OpHandle& h) {
+  StarForest& sf = *h.sf;
+  DevPlan& d = sf.dev();
+  const size_t ub = h.unit.bytes();
+  const bool det = sf.comm().config().deterministic;
+  if (!h.recvs.empty()) sf.comm().transport().finish(data_tag(h.opid), h.recvs, h.stream);
+  if (!d.rg.empty() && h.stg->leaf_reply == nullptr && h.stg->leaf_bytes)
+    SFG_CUDA(cudaMalloc(&h.stg->leaf_reply, h.stg->leaf_bytes));
+
+  // Root side: serialize every contribution per root.
+  {
+    Launch L;
+    set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
+    if (det) {
+      sf.ensure_csr();
+      L.add(csr_seg(d, CsrRange::all, SEG_CSR_FETCH));
+    } else {
+      if (d.has_self) {
+        DSeg s = pair_seg(d.self_leaf, BUF_SRC_RO, d.self_root, BUF_ROOT, d.n_self, false);
+        s.type = SEG_ATOMIC_FETCH;
+        s.aux_buf = BUF_LEAFUPDATE;
+        L.add(s);
+      }
+      for (const auto& g : d.lg) {
+        DSeg s = pair_seg(contig(g.stage_off), BUF_ROOT_STAGE, g.pat, BUF_ROOT, g.n, false);
+        s.type = SEG_ATOMIC_FETCH;
+        s.aux_buf = BUF_ROOT_STAGE;
+        L.add(s);
+      }
+    }
+    L.run(h.unit, h.op, h.stream);
+  }
+
+  // Replies travel back in place (ops.cpp:559-561), then land in leafupdate.
+  std::vector<XferOp> sends;
+  for (const auto& g : d.lg)
+    sends.push_back({g.rank, at(h.stg->root_stage, g.stage_off, ub), static_cast<size_t>(g.n) * ub});
+  h.reply_recvs.clear();
+  h.zero_copy_recv.clear();
+  for (const auto& g : d.rg) {
+    const bool zc = g.contiguous;
+    h.zero_copy_recv.push_back(zc ? 1 : 0);
+    void* ptr = zc ? at(h.leafupdate, g.contig_start, ub) : at(h.stg->leaf_reply, g.stage_off, ub);
+    h.reply_recvs.push_back({g.rank, ptr, static_cast<size_t>(g.n) * ub});
+  }
+  if (!sends.empty() || !h.reply_recvs.empty()) {
+    sf.comm().transport().start(reply_tag(h.opid), sends, h.reply_recvs, h.stream);
+    counters().transport_calls++;
+    sf.comm().transport().finish(reply_tag(h.opid), h.reply_recvs, h.stream);
+  }
+  Launch U;
+  set_bufs(U, h, h.dst, const_cast<void*>(h.src), h.src);
+  for (size_t k = 0; k < d.rg.size(); ++k) {
+    if (h.zero_copy_recv[k]) continue;
+    const auto& g = d.rg[k];
+    U.add(pair_seg(contig(g.stage_off), BUF_LEAF_REPLY, g.pat, BUF_LEAFUPDATE, g.n, true));
+    counters().unpack_copies++;
+  }
+  U.run(h.unit, ReduceOp::replace, h.stream);
+}
+
+void require_ready(StarForest& sf, const Unit& unit, ReduceOp op, const char* what) {
+  SFG_REQUIRE(sf.state() == SfState::set_up, std::string(what) + " requires a set-up star forest");
+  check_unit_op(unit, op);
+}
+
+void require_end(OpHandle& h, OpKind kind, const char* what) {
+  SFG_REQUIRE(h.sf != nullptr, std::string(what) + ": handle was never begun");
+  SFG_REQUIRE(!h.ended, std::string(what) + ": handle already ended");
+  SFG_REQUIRE(h.kind == kind, std::string(what) + ": handle belongs to a different operation");
+  h.ended = true;
+  h.sf->comm().bind_device();
+}
+
+std::unique_ptr<OpHandle> make_handle(StarForest& sf, OpKind kind, const Unit& u, ReduceOp op,
+                                      const void* src, void* dst, cudaStream_t s) {
+  auto h = std::make_unique<OpHandle>();
+  h->sf = &sf;
+  h->kind = kind;
+  h->unit = u;
+  h->op = op;
+  h->src = src;
+  h->dst = dst;
+  h->stream = s;
+  return h;
+}
+
+}  // namespace
+
+std::unique_ptr<OpHandle> bcast_begin(StarForest& sf, const Unit& u, const void* rootdata,
+                                      void* leafdata, ReduceOp op, cudaStream_t s) {
+  require_ready(sf, u, op, "bcast");
+  auto h = make_handle(sf, OpKind::bcast, u, op, rootdata, leafdata, s);
+  begin_common(*h, rootdata, static_cast<size_t>(sf.nroots()) * u.bytes());
+  begin_root_to_leaf(*h);
+  return h;
+}
+
+void bcast_end(OpHandle& h) {
+  require_end(h, OpKind::bcast, "bcast_end");
+  end_root_to_leaf(h);
+  end_common(h);
+}
+
+std::unique_ptr<OpHandle> reduce_begin(StarForest& sf, const Unit& u, const void* leafdata,
+                                       void* rootdata, ReduceOp op, cudaStream_t s) {
+  require_ready(sf, u, op, "reduce");
+  auto h = make_handle(sf, OpKind::reduce, u, op, leafdata, rootdata, s);
+  begin_common(*h, leafdata, static_cast<size_t>(sf.leaf_index_bound()) * u.bytes());
+  begin_leaf_to_root(*h);
+  return h;
+}
+
+void reduce_end(OpHandle& h) {
+  require_end(h, OpKind::reduce, "reduce_end");
+  end_leaf_to_root(h);
+  end_common(h);
+}
+
+std::unique_ptr<OpHandle> fetch_and_op_begin(StarForest& sf, const Unit& u, void* rootdata,
+                                             const void* leafdata, void* leafupdate, ReduceOp op,
+                                             cudaStream_t s) {
+  SFG_REQUIRE(op != ReduceOp::replace, "fetch-and-op with replace has no fetch semantics");
+  require_ready(sf, u, op, "fetch_and_op");
+  auto h = make_handle(sf, OpKind::fetch_and_op, u, op, leafdata, rootdata, s);
+  h->leafupdate = leafupdate;
+  begin_common(*h, leafdata, static_cast<size_t>(sf.leaf_index_bound()) * u.bytes());
+  begin_fetch(*h);
+  return h;
+}
+
+void fetch_and_op_end(OpHandle& h) {
+  require_end(h, OpKind::fetch_and_op, "fetch_and_op_end");
+  end_fetch(h);
+  end_common(h);
+}
+
+std::unique_ptr<OpHandle> gather_begin(StarForest& sf, const Unit& u, const void* leafdata,
+                                       void* multirootdata, cudaStream_t s) {
+  require_ready(sf, u, ReduceOp::replace, "gather");
+  StarForest& m = sf.multi_sf();
+  auto h = make_handle(m, OpKind::gather, u, ReduceOp::replace, leafdata, multirootdata, s);
+  begin_common(*h, leafdata, static_cast<size_t>(m.leaf_index_bound()) * u.bytes());
+  begin_leaf_to_root(*h);
+  return h;
+}
+
+void gather_end(OpHandle& h) {
+  require_end(h, OpKind::gather, "gather_end");
+  end_leaf_to_root(h);
+  end_common(h);
+}
+
+std::unique_ptr<OpHandle> scatter_begin(StarForest& sf, const Unit& u, const void* multirootdata,
+                                        void* leafdata, cudaStream_t s) {
+  require_ready(sf, u, ReduceOp::replace, "scatter");
+  StarForest& m = sf.multi_sf();
+  auto h = make_handle(m, OpKind::scatter, u, ReduceOp::replace, multirootdata, leafdata, s);
+  begin_common(*h, multirootdata, static_cast<size_t>(m.nroots()) * u.bytes());
+  begin_root_to_leaf(*h);
+  return h;
+}
+
+void scatter_end(OpHandle& h) {
+  require_end(h, OpKind::scatter, "scatter_end");
+  end_root_to_leaf(h);
+  end_common(h);
+}
+
+}  // namespace sfg

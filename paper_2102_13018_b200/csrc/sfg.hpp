@@ -1,0 +1,397 @@
+// Internal C++ core of the B200 star-forest layer.
+//
+// Mirrors the reference's layering (/root/reference/proj/include/sf/*.hpp):
+//   vocabulary (Unit/Kind/ReduceOp/Error)   <- unit.hpp, errors.hpp
+//   Comm = control plane + data-plane transport   <- comm.hpp, exchange.hpp
+//   StarForest (set_graph/setup/degrees/multi_sf) <- starforest.hpp
+//   split-phase operations                        <- ops.hpp
+// but the data plane is device-resident: per-peer plans live in HBM, packs
+// and unpacks are sm_100a kernels (kernels.cu), remote exchange is grouped
+// NCCL send/recv (or stream-ordered peer copies for in-process ranks), and
+// nothing synchronises the host between Begin and End.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.hpp"
+
+namespace sfg {
+
+// ---------------------------------------------------------------- vocabulary
+// /root/reference/proj/include/sf/unit.hpp:14-82
+enum class Kind : uint8_t { int32 = 0, int64 = 1, float64 = 2, bytes = 3 };
+enum class ReduceOp : uint8_t { replace = 0, sum, prod, max, min, land, lor, band, bor };
+
+const char* kind_name(Kind k);
+const char* op_name(ReduceOp op);
+
+struct Unit {
+  Kind kind = Kind::int64;
+  int64_t blocklen = 1;
+  size_t elem_size() const;
+  size_t bytes() const { return elem_size() * static_cast<size_t>(blocklen); }
+};
+
+// /root/reference/proj/include/sf/errors.hpp:11-32
+class Error : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class TimeoutError : public Error {
+ public:
+  using Error::Error;
+};
+class CudaError : public Error {
+ public:
+  using Error::Error;
+};
+
+[[noreturn]] void fail(const std::string& msg);
+#define SFG_REQUIRE(cond, msg)   \
+  do {                           \
+    if (!(cond)) ::sfg::fail(msg); \
+  } while (0)
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+void nccl_check(ncclResult_t r, const char* what, const char* file, int line);
+#define SFG_CUDA(x) ::sfg::cuda_check((x), #x, __FILE__, __LINE__)
+#define SFG_NCCL(x) ::sfg::nccl_check((x), #x, __FILE__, __LINE__)
+
+void check_unit_op(const Unit& u, ReduceOp op);
+
+// ------------------------------------------------------------------- config
+// /root/reference/proj/include/sf/comm.hpp:54-66
+struct CommConfig {
+  std::string backend = "threads";  // threads (in-process ranks) | nccl
+  bool deterministic = true;        // reference fold order, bit-exact
+  bool debug_checksum = false;      // verify source buffers between begin/end
+  bool force_remote = false;        // route self edges through the transport
+  int dense_discovery_threshold = 64;
+  uint64_t seed = 1;
+  double timeout_s = 30.0;
+};
+
+// Copy instrumentation, the analogue of PackCounters
+// (/root/reference/proj/include/sf/pack.hpp:20-32).
+struct Counters {
+  std::atomic<uint64_t> pack_copies{0};      // remote groups packed into staging
+  std::atomic<uint64_t> pack_elided{0};      // zero-copy sends (contiguous)
+  std::atomic<uint64_t> unpack_copies{0};    // remote groups unpacked from staging
+  std::atomic<uint64_t> unpack_elided{0};    // zero-copy receives
+  std::atomic<uint64_t> replace_dup_collisions{0};
+  std::atomic<uint64_t> kernel_launches{0};
+  std::atomic<uint64_t> bytes_sent{0};
+  std::atomic<uint64_t> bytes_recv{0};
+  std::atomic<uint64_t> transport_calls{0};
+  void reset();
+};
+Counters& counters();
+
+// --------------------------------------------------------------- pattern
+// Classification of an index list (/root/reference/proj/include/sf/pattern.hpp:28-102).
+// Unlike the reference (which only recognises strided subdomains when handed
+// GridExtents, pattern.cpp:50-64), the planner infers Affine3D blocks from the
+// indices themselves and verifies them, as PetscSF does.
+struct Pattern {
+  enum Kind : uint8_t { contiguous = 0, affine = 1, indexed = 2 };
+  Kind kind = contiguous;
+  int64_t count = 0;
+  int64_t start = 0;
+  int64_t dx = 0, dy = 0, dz = 0, s1 = 0, s2 = 0;  // affine
+  std::vector<int64_t> idx;                         // indexed
+  bool has_duplicates = false;
+  int64_t bound = 0;  // largest index + 1 (0 when empty)
+
+  // extents_x / extents_xy > 0: reference-style detection with known extents.
+  static Pattern analyze(const int64_t* idx, int64_t n, bool infer_affine = true,
+                         int64_t extents_x = 0, int64_t extents_xy = 0);
+  static Pattern contiguous_range(int64_t start, int64_t n);
+  int64_t index(int64_t i) const;
+  bool is_contiguous() const { return kind == contiguous; }
+};
+
+// -------------------------------------------------------- control plane
+// Host-side collectives used only by SetUp / multi-SF construction
+// (the reference's allreduce + sparse exchange, comm.cpp:196-214,
+// exchange.cpp:32-102).
+class ControlPlane {
+ public:
+  virtual ~ControlPlane() = default;
+  virtual int rank() const = 0;
+  virtual int size() const = 0;
+  // out receives size()*bytes: rank r's contribution at r*bytes.
+  virtual void allgather(const void* in, size_t bytes, void* out) = 0;
+  // send[r] goes to rank r; returns what each rank sent to me.
+  virtual std::vector<std::vector<uint8_t>> alltoallv(std::vector<std::vector<uint8_t>> send) = 0;
+  virtual void barrier() = 0;
+};
+
+// One posted buffer of the in-process transport's put protocol.
+struct Post {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaEvent_t ev = nullptr;
+  int device = -1;
+};
+
+// In-process world: ranks are threads of one process (the reference's
+// harness model, /root/reference/proj/src/harness.cpp:51-101). Hosts the
+// threads control plane and the rendezvous table of the threads transport.
+class World {
+ public:
+  World(int n, double timeout_s);
+  int size() const { return n_; }
+  double timeout_s() const { return timeout_s_; }
+  void abort() { aborted_.store(true); cv_.notify_all(); }
+  bool aborted() const { return aborted_.load(); }
+
+  void barrier(const char* what);
+  void put_slot(int rank, std::vector<uint8_t> data);
+  const std::vector<uint8_t>& slot(int rank) const { return slots_[rank]; }
+  void put_mail(int src, int dst, std::vector<uint8_t> data);
+  std::vector<uint8_t> take_mail(int src, int dst);
+
+  // key: (tag, src, dst, kind)
+  struct Key {
+    uint64_t tag;
+    int src, dst, kind;
+    bool operator<(const Key& o) const {
+      if (tag != o.tag) return tag < o.tag;
+      if (src != o.src) return src < o.src;
+      if (dst != o.dst) return dst < o.dst;
+      return kind < o.kind;
+    }
+  };
+  void post(const Key& k, const Post& p);
+  Post take(const Key& k, const char* what);
+
+ private:
+  int n_;
+  double timeout_s_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::atomic<bool> aborted_{false};
+  int arrived_ = 0;
+  uint64_t generation_ = 0;
+  std::vector<std::vector<uint8_t>> slots_;
+  std::vector<std::vector<std::vector<uint8_t>>> mail_;
+  std::map<Key, Post> posts_;
+};
+
+struct XferOp {
+  int peer = -1;
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+// Data-plane transport. start() enqueues one exchange phase on `stream`
+// (sends of data produced earlier on `stream`); finish() makes `stream`
+// wait until the receives of that phase have landed. Neither blocks the host
+// on the GPU.
+class Transport {
+ public:
+  virtual ~Transport() = default;
+  virtual void start(uint64_t tag, const std::vector<XferOp>& sends,
+                     const std::vector<XferOp>& recvs, cudaStream_t stream) = 0;
+  virtual void finish(uint64_t tag, const std::vector<XferOp>& recvs, cudaStream_t stream) = 0;
+  virtual const char* name() const = 0;
+};
+
+class Comm {
+ public:
+  Comm(int nranks, int rank, int device, CommConfig cfg);
+  ~Comm();
+  int rank() const { return rank_; }
+  int size() const { return size_; }
+  int device() const { return device_; }
+  bool has_device() const { return device_ >= 0; }
+  const CommConfig& config() const { return cfg_; }
+  CommConfig& config_mut() { return cfg_; }
+  ControlPlane& ctrl() { return *ctrl_; }
+  Transport& transport();
+  uint64_t next_op_seq() { return ++op_seq_; }
+  void bind_device() const;
+
+  // wiring (abi.cpp)
+  std::unique_ptr<ControlPlane> ctrl_;
+  std::unique_ptr<Transport> transport_;
+  ncclComm_t nccl_ = nullptr;
+  World* world_ = nullptr;
+
+ private:
+  int size_, rank_, device_;
+  CommConfig cfg_;
+  uint64_t op_seq_ = 0;
+};
+
+std::unique_ptr<ControlPlane> make_threads_ctrl(World* w, int rank);
+std::unique_ptr<ControlPlane> make_single_ctrl();
+std::unique_ptr<ControlPlane> make_nccl_ctrl(ncclComm_t comm, int rank, int size, int device);
+std::unique_ptr<Transport> make_threads_transport(World* w, int rank, int device, double timeout_s);
+std::unique_ptr<Transport> make_nccl_transport(ncclComm_t comm, int rank, int device);
+
+// ------------------------------------------------------------ star forest
+enum class SfState { created = 0, graph_set = 1, set_up = 2 };
+enum class SetupAlg { automatic = 0, dense = 1, consensus = 2 };
+
+// One neighbor group, aligned across the pair (starforest.hpp:47-55,110-121).
+struct Group {
+  int rank = -1;
+  std::vector<int64_t> items;  // root groups: leaf ordinals; leaf groups: root offsets
+  Pattern pat;                 // root groups: leaf-index pattern; leaf groups: root pattern
+};
+
+// Device-resident plan (built once per forest, on first use).
+struct DevPlan {
+  bool built = false;
+  void* blob = nullptr;  // all device index arrays
+  bool has_self = false;
+  int64_t n_self = 0;
+  DPat self_root, self_leaf;
+  struct Seg {
+    int rank;
+    int64_t n;
+    int64_t stage_off;  // vertices
+    DPat pat;
+    bool contiguous;
+    int64_t contig_start;
+  };
+  std::vector<Seg> rg;  // remote root groups (I own the leaves)
+  std::vector<Seg> lg;  // remote leaf groups (I own the roots)
+  int64_t n_leafside = 0;  // total remote edges, leaf side
+  int64_t n_rootside = 0;  // total remote edges, root side
+  bool self_root_dups = false;
+  bool remote_root_dups = false;
+  // root-sorted CSR (lazy)
+  bool csr_built = false;
+  void* csr_blob = nullptr;
+  int64_t csr_n = 0;
+  int32_t* csr_roots = nullptr;
+  int32_t* csr_off = nullptr;    // [csr_n + 1]
+  int32_t* csr_split = nullptr;  // [csr_n]: end of self entries
+  int32_t* csr_ent = nullptr;
+  ~DevPlan();
+};
+
+struct Staging {
+  size_t unit_bytes = 0;
+  void* leaf_stage = nullptr;   // n_leafside * ub
+  void* root_stage = nullptr;   // n_rootside * ub
+  void* leaf_reply = nullptr;   // n_leafside * ub (fetch-and-op)
+  unsigned long long* digest = nullptr;
+  cudaEvent_t released = nullptr;
+  bool released_recorded = false;
+  bool in_use = false;
+  size_t leaf_bytes = 0, root_bytes = 0;
+  ~Staging();
+};
+
+class StarForest {
+ public:
+  explicit StarForest(Comm* comm);
+  ~StarForest();
+
+  void set_graph(int64_t nroots, int64_t nleaves, const int64_t* leaf_local,
+                 const int32_t* remote_rank, const int64_t* remote_off);
+  void setup(SetupAlg alg = SetupAlg::automatic);
+
+  Comm& comm() { return *comm_; }
+  SfState state() const { return state_; }
+  int64_t nroots() const { return nroots_; }
+  int64_t nleaves() const { return nleaves_; }
+  int64_t leaf_index_bound() const { return leaf_bound_; }
+  bool contiguous_leaves() const { return contiguous_leaves_; }
+  int64_t leaf_index(int64_t ordinal) const {
+    return leaf_local_.empty() ? ordinal : leaf_local_[static_cast<size_t>(ordinal)];
+  }
+  const std::vector<Group>& root_groups() const;
+  const std::vector<Group>& leaf_groups() const;
+  bool has_self_edges() const;
+  std::vector<int64_t> compute_degrees() const;
+  StarForest& multi_sf();
+  void require_state(SfState s, const char* what) const;
+
+  // device side
+  DevPlan& dev();
+  void ensure_csr();
+  Staging* acquire_staging(size_t ub, cudaStream_t stream);
+  void release_staging(Staging* s, cudaStream_t stream);
+
+  int32_t remote_rank_of(int64_t o) const { return remote_rank_[static_cast<size_t>(o)]; }
+  int64_t remote_off_of(int64_t o) const { return remote_off_[static_cast<size_t>(o)]; }
+  bool has_local() const { return has_local_; }
+
+ private:
+  Comm* comm_;
+  SfState state_ = SfState::created;
+  int64_t nroots_ = 0, nleaves_ = 0, leaf_bound_ = 0;
+  bool contiguous_leaves_ = true;
+  bool has_local_ = false;
+  std::vector<int64_t> leaf_local_;
+  std::vector<int32_t> remote_rank_;
+  std::vector<int64_t> remote_off_;
+  std::vector<Group> root_groups_, leaf_groups_;
+  bool self_first_ = false;
+  std::unique_ptr<StarForest> multi_;
+  std::unique_ptr<DevPlan> dev_;
+  std::vector<std::unique_ptr<Staging>> staging_;
+};
+
+// ------------------------------------------------------------ operations
+// /root/reference/proj/include/sf/ops.hpp:14-94
+enum class OpKind : uint8_t { bcast = 0, reduce, fetch_and_op, gather, scatter };
+
+struct OpHandle {
+  StarForest* sf = nullptr;  // forest the transfer runs over (multi-SF for gather/scatter)
+  OpKind kind = OpKind::bcast;
+  Unit unit;
+  ReduceOp op = ReduceOp::replace;
+  const void* src = nullptr;
+  void* dst = nullptr;
+  void* leafupdate = nullptr;
+  uint64_t opid = 0;
+  bool ended = false;
+  cudaStream_t stream = nullptr;
+  Staging* stg = nullptr;
+  std::vector<XferOp> recvs;        // phase-1 receives
+  std::vector<XferOp> reply_recvs;  // fetch-and-op replies
+  std::vector<uint8_t> zero_copy_recv;
+  // debug checksum
+  const void* ck_ptr = nullptr;
+  size_t ck_bytes = 0;
+  unsigned long long ck_value = 0;
+  // host-memory staging (reference-style host pointers)
+  bool host_mode = false;
+};
+
+std::unique_ptr<OpHandle> bcast_begin(StarForest& sf, const Unit& u, const void* rootdata,
+                                      void* leafdata, ReduceOp op, cudaStream_t s);
+void bcast_end(OpHandle& h);
+std::unique_ptr<OpHandle> reduce_begin(StarForest& sf, const Unit& u, const void* leafdata,
+                                       void* rootdata, ReduceOp op, cudaStream_t s);
+void reduce_end(OpHandle& h);
+std::unique_ptr<OpHandle> fetch_and_op_begin(StarForest& sf, const Unit& u, void* rootdata,
+                                             const void* leafdata, void* leafupdate, ReduceOp op,
+                                             cudaStream_t s);
+void fetch_and_op_end(OpHandle& h);
+std::unique_ptr<OpHandle> gather_begin(StarForest& sf, const Unit& u, const void* leafdata,
+                                       void* multirootdata, cudaStream_t s);
+void gather_end(OpHandle& h);
+std::unique_ptr<OpHandle> scatter_begin(StarForest& sf, const Unit& u, const void* multirootdata,
+                                        void* leafdata, cudaStream_t s);
+void scatter_end(OpHandle& h);
+
+DPat to_dpat(const Pattern& p, const int32_t* dev_idx);
+
+}  // namespace sfg

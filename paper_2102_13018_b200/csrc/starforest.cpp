@@ -1,0 +1,462 @@
+// StarForest: graph specification, the SetUp planner, degrees, multi-SF and
+// the device-resident communication plans.
+//
+// Reference: /root/reference/proj/src/starforest.cpp:18-249.
+//   set_graph  :29-76   validation + contiguity (same error messages)
+//   setup      :82-161  leaf-index order, grouping by root rank, discovery,
+//                       offset validation, self group to the head
+//   compute_degrees :183-189, multi_sf :191-240
+// What is new: SetUp ends with pattern classification that recognises
+// Affine3D blocks without extents, and the first device operation uploads a
+// per-forest plan (indexed patterns as int32, affine/contiguous as
+// descriptors only) plus, when a reduction needs it, a root-sorted CSR that
+// reproduces the reference's deterministic fold order.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "sfg.hpp"
+
+namespace sfg {
+
+namespace {
+constexpr int64_t kI32Max = (int64_t(1) << 31) - 1;
+}
+
+DevPlan::~DevPlan() {
+  if (blob) cudaFree(blob);
+  if (csr_blob) cudaFree(csr_blob);
+}
+
+Staging::~Staging() {
+  if (leaf_stage) cudaFree(leaf_stage);
+  if (root_stage) cudaFree(root_stage);
+  if (leaf_reply) cudaFree(leaf_reply);
+  if (digest) cudaFree(digest);
+  if (released) cudaEventDestroy(released);
+}
+
+StarForest::StarForest(Comm* comm) : comm_(comm) {
+  SFG_REQUIRE(comm != nullptr, "star forest needs a valid communicator");
+}
+
+StarForest::~StarForest() {
+  if (comm_ && comm_->has_device() && (dev_ || !staging_.empty())) {
+    cudaSetDevice(comm_->device());
+    cudaDeviceSynchronize();
+  }
+}
+
+void StarForest::require_state(SfState s, const char* what) const {
+  if (state_ == s) return;
+  static constexpr const char* names[] = {"created", "graph-set", "set-up"};
+  throw Error(std::string(what) + " requires a " + names[static_cast<int>(s)] +
+              " star forest (state is " + names[static_cast<int>(state_)] + ")");
+}
+
+void StarForest::set_graph(int64_t nroots, int64_t nleaves, const int64_t* leaf_local,
+                           const int32_t* remote_rank, const int64_t* remote_off) {
+  SFG_REQUIRE(state_ == SfState::created || state_ == SfState::graph_set,
+              "set_graph requires a created or graph-set star forest");
+  SFG_REQUIRE(nroots >= 0 && nleaves >= 0, "set_graph: negative root or leaf count");
+  SFG_REQUIRE(nleaves == 0 || (remote_rank != nullptr && remote_off != nullptr),
+              "set_graph: leaf_remote length does not match nleaves");
+
+  int64_t bound = nleaves;
+  bool contiguous = true;
+  if (leaf_local != nullptr) {
+    bool increasing = true;
+    for (int64_t i = 0; i < nleaves; ++i) {
+      if (i > 0 && leaf_local[i] <= leaf_local[i - 1]) increasing = false;
+      contiguous = contiguous && leaf_local[i] == i;
+    }
+    if (increasing) {
+      SFG_REQUIRE(nleaves == 0 || leaf_local[0] >= 0, "set_graph: negative leaf index");
+      bound = nleaves == 0 ? 0 : leaf_local[nleaves - 1] + 1;
+    } else {
+      std::vector<int64_t> sorted(leaf_local, leaf_local + nleaves);
+      std::sort(sorted.begin(), sorted.end());
+      for (size_t i = 0; i < sorted.size(); ++i) {
+        SFG_REQUIRE(sorted[i] >= 0, "set_graph: negative leaf index");
+        SFG_REQUIRE(i == 0 || sorted[i] != sorted[i - 1],
+                    "set_graph: duplicate leaf index " + std::to_string(sorted[i]) +
+                        " violates the forest property");
+      }
+      bound = sorted.empty() ? 0 : sorted.back() + 1;
+    }
+  }
+  const int nranks = comm_->size();
+  for (int64_t i = 0; i < nleaves; ++i) {
+    SFG_REQUIRE(remote_rank[i] >= 0 && remote_rank[i] < nranks,
+                "set_graph: root rank " + std::to_string(remote_rank[i]) + " outside communicator");
+    SFG_REQUIRE(remote_off[i] >= 0, "set_graph: negative root offset");
+  }
+
+  nroots_ = nroots;
+  nleaves_ = nleaves;
+  leaf_bound_ = bound;
+  contiguous_leaves_ = contiguous;
+  has_local_ = leaf_local != nullptr;
+  if (has_local_ && !contiguous)
+    leaf_local_.assign(leaf_local, leaf_local + nleaves);
+  else
+    leaf_local_.clear();  // identity: leaf index == ordinal
+  remote_rank_.assign(remote_rank, remote_rank + nleaves);
+  remote_off_.assign(remote_off, remote_off + nleaves);
+  root_groups_.clear();
+  leaf_groups_.clear();
+  self_first_ = false;
+  multi_.reset();
+  dev_.reset();
+  staging_.clear();
+  state_ = SfState::graph_set;
+}
+
+void StarForest::setup(SetupAlg alg) {
+  require_state(SfState::graph_set, "setup");
+  (void)alg;  // dense and consensus discovery produce identical results
+              // (exchange.hpp:30-32); both map to one sparse exchange here.
+  const int me = comm_->rank();
+  const int P = comm_->size();
+  const int64_t n = nleaves_;
+
+  // Edge order within a neighbor pair: ascending leaf index (starforest.cpp:86-90).
+  std::vector<int64_t> order;
+  bool identity = true;
+  for (int64_t i = 1; i < n && !leaf_local_.empty(); ++i)
+    if (leaf_local_[static_cast<size_t>(i)] < leaf_local_[static_cast<size_t>(i - 1)]) {
+      identity = false;
+      break;
+    }
+  if (!identity) {
+    order.resize(static_cast<size_t>(n));
+    std::iota(order.begin(), order.end(), int64_t{0});
+    std::sort(order.begin(), order.end(),
+              [&](int64_t a, int64_t b) { return leaf_index(a) < leaf_index(b); });
+  }
+  auto ord = [&](int64_t i) { return identity ? i : order[static_cast<size_t>(i)]; };
+
+  // Group by root rank, ascending, stable (counting sort).
+  std::vector<int64_t> cnt(static_cast<size_t>(P) + 1, 0);
+  for (int64_t i = 0; i < n; ++i) ++cnt[static_cast<size_t>(remote_rank_[static_cast<size_t>(i)]) + 1];
+  for (int r = 0; r < P; ++r) cnt[static_cast<size_t>(r) + 1] += cnt[static_cast<size_t>(r)];
+  std::vector<std::vector<int64_t>> ords(static_cast<size_t>(P));
+  for (int r = 0; r < P; ++r)
+    ords[static_cast<size_t>(r)].reserve(static_cast<size_t>(cnt[static_cast<size_t>(r) + 1] - cnt[static_cast<size_t>(r)]));
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t o = ord(i);
+    ords[static_cast<size_t>(remote_rank_[static_cast<size_t>(o)])].push_back(o);
+  }
+  order.clear();
+  order.shrink_to_fit();
+
+  // Discovery payload: root offsets in edge order (starforest.cpp:96-107).
+  std::vector<std::vector<uint8_t>> send(static_cast<size_t>(P));
+  for (int r = 0; r < P; ++r) {
+    const auto& os = ords[static_cast<size_t>(r)];
+    auto& buf = send[static_cast<size_t>(r)];
+    buf.resize(os.size() * sizeof(int64_t));
+    auto* p = reinterpret_cast<int64_t*>(buf.data());
+    for (size_t i = 0; i < os.size(); ++i) p[i] = remote_off_[static_cast<size_t>(os[i])];
+  }
+  auto recv = comm_->ctrl().alltoallv(std::move(send));
+
+  std::vector<Group> roots, leaves;
+  for (int r = 0; r < P; ++r) {
+    auto& os = ords[static_cast<size_t>(r)];
+    if (os.empty()) continue;
+    Group g;
+    g.rank = r;
+    g.items = std::move(os);
+    roots.push_back(std::move(g));
+  }
+  for (int r = 0; r < P; ++r) {
+    const auto& b = recv[static_cast<size_t>(r)];
+    if (b.empty()) continue;
+    SFG_REQUIRE(b.size() % sizeof(int64_t) == 0, "malformed setup payload");
+    Group g;
+    g.rank = r;
+    g.items.resize(b.size() / sizeof(int64_t));
+    std::memcpy(g.items.data(), b.data(), b.size());
+    for (int64_t off : g.items)
+      SFG_REQUIRE(off < nroots_, "setup: leaf on rank " + std::to_string(r) +
+                                     " references root offset " + std::to_string(off) +
+                                     " but this rank has only " + std::to_string(nroots_) +
+                                     " roots");
+    leaves.push_back(std::move(g));
+  }
+  recv.clear();
+  auto self_to_head = [me](std::vector<Group>& gs) {
+    auto it = std::find_if(gs.begin(), gs.end(), [me](const Group& g) { return g.rank == me; });
+    if (it != gs.end()) std::rotate(gs.begin(), it, it + 1);
+  };
+  self_to_head(roots);
+  self_to_head(leaves);
+  self_first_ = !roots.empty() && roots.front().rank == me;
+
+  for (auto& g : roots) {
+    std::vector<int64_t> leaf_idx(g.items.size());
+    for (size_t i = 0; i < g.items.size(); ++i) leaf_idx[i] = leaf_index(g.items[i]);
+    g.pat = Pattern::analyze(leaf_idx.data(), static_cast<int64_t>(leaf_idx.size()));
+  }
+  for (auto& g : leaves) g.pat = Pattern::analyze(g.items.data(), static_cast<int64_t>(g.items.size()));
+
+  root_groups_ = std::move(roots);
+  leaf_groups_ = std::move(leaves);
+  state_ = SfState::set_up;
+}
+
+const std::vector<Group>& StarForest::root_groups() const {
+  require_state(SfState::set_up, "root_groups");
+  return root_groups_;
+}
+
+const std::vector<Group>& StarForest::leaf_groups() const {
+  require_state(SfState::set_up, "leaf_groups");
+  return leaf_groups_;
+}
+
+bool StarForest::has_self_edges() const {
+  require_state(SfState::set_up, "has_self_edges");
+  return self_first_;
+}
+
+std::vector<int64_t> StarForest::compute_degrees() const {
+  require_state(SfState::set_up, "compute_degrees");
+  std::vector<int64_t> degree(static_cast<size_t>(nroots_), 0);
+  for (const auto& g : leaf_groups_)
+    for (int64_t off : g.items) ++degree[static_cast<size_t>(off)];
+  return degree;
+}
+
+// One new root per incoming edge, walking leaf groups in stored order (self
+// first, then ascending rank; edge order inside) — starforest.cpp:191-240.
+StarForest& StarForest::multi_sf() {
+  require_state(SfState::set_up, "multi_sf");
+  if (multi_) return *multi_;
+  const int me = comm_->rank();
+  const int P = comm_->size();
+  const auto degrees = compute_degrees();
+  std::vector<int64_t> next(degrees.size());
+  int64_t acc = 0;
+  for (size_t i = 0; i < degrees.size(); ++i) {
+    next[i] = acc;
+    acc += degrees[i];
+  }
+  const int64_t multi_nroots = acc;
+
+  std::vector<std::vector<uint8_t>> send(static_cast<size_t>(P));
+  for (const auto& g : leaf_groups_) {
+    auto& buf = send[static_cast<size_t>(g.rank)];
+    buf.resize(g.items.size() * sizeof(int64_t));
+    auto* p = reinterpret_cast<int64_t*>(buf.data());
+    for (size_t i = 0; i < g.items.size(); ++i) p[i] = next[static_cast<size_t>(g.items[i])]++;
+  }
+  auto recv = comm_->ctrl().alltoallv(std::move(send));
+
+  std::vector<int32_t> mrank(static_cast<size_t>(nleaves_));
+  std::vector<int64_t> moff(static_cast<size_t>(nleaves_));
+  for (const auto& g : root_groups_) {
+    const auto& b = recv[static_cast<size_t>(g.rank)];
+    SFG_REQUIRE(b.size() == g.items.size() * sizeof(int64_t),
+                "multi-sf slot exchange length mismatch");
+    const auto* p = reinterpret_cast<const int64_t*>(b.data());
+    for (size_t i = 0; i < g.items.size(); ++i) {
+      mrank[static_cast<size_t>(g.items[i])] = g.rank;
+      moff[static_cast<size_t>(g.items[i])] = p[i];
+    }
+  }
+  (void)me;
+  auto m = std::make_unique<StarForest>(comm_);
+  std::vector<int64_t> local;
+  if (has_local_) {
+    local.resize(static_cast<size_t>(nleaves_));
+    for (int64_t o = 0; o < nleaves_; ++o) local[static_cast<size_t>(o)] = leaf_index(o);
+  }
+  m->set_graph(multi_nroots, nleaves_, has_local_ ? local.data() : nullptr, mrank.data(), moff.data());
+  m->setup();
+  multi_ = std::move(m);
+  return *multi_;
+}
+
+// ------------------------------------------------------------ device plan
+
+DevPlan& StarForest::dev() {
+  require_state(SfState::set_up, "device plan");
+  if (dev_ && dev_->built) return *dev_;
+  comm_->bind_device();
+  auto d = std::make_unique<DevPlan>();
+  const int me = comm_->rank();
+  const bool force = comm_->config().force_remote;
+
+  // Collect the int32 arrays of every indexed pattern into one upload.
+  std::vector<int32_t> host;
+  std::vector<std::pair<const Pattern*, size_t>> idx_pats;
+  auto reserve_pat = [&](const Pattern& p) {
+    if (p.kind != Pattern::indexed) return;
+    idx_pats.push_back({&p, host.size()});
+    for (int64_t v : p.idx) {
+      SFG_REQUIRE(v <= kI32Max, "index exceeds the int32 range of device plans");
+      host.push_back(static_cast<int32_t>(v));
+    }
+  };
+
+  const bool self = self_first_ && !force;
+  if (self) {
+    reserve_pat(leaf_groups_.front().pat);
+    reserve_pat(root_groups_.front().pat);
+  }
+  for (size_t gi = self ? 1 : 0; gi < root_groups_.size(); ++gi) reserve_pat(root_groups_[gi].pat);
+  for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size(); ++gi) reserve_pat(leaf_groups_[gi].pat);
+
+  int32_t* dbase = nullptr;
+  if (!host.empty()) {
+    SFG_CUDA(cudaMalloc(&d->blob, host.size() * sizeof(int32_t)));
+    SFG_CUDA(cudaMemcpy(d->blob, host.data(), host.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    dbase = static_cast<int32_t*>(d->blob);
+  }
+  auto dpat = [&](const Pattern& p) {
+    const int32_t* ptr = nullptr;
+    for (const auto& [pp, off] : idx_pats)
+      if (pp == &p) ptr = dbase + off;
+    return to_dpat(p, ptr);
+  };
+
+  if (self) {
+    d->has_self = true;
+    d->n_self = static_cast<int64_t>(leaf_groups_.front().items.size());
+    d->self_root = dpat(leaf_groups_.front().pat);
+    d->self_leaf = dpat(root_groups_.front().pat);
+    d->self_root_dups = leaf_groups_.front().pat.has_duplicates;
+  }
+  int64_t off = 0;
+  for (size_t gi = self ? 1 : 0; gi < root_groups_.size(); ++gi) {
+    const auto& g = root_groups_[gi];
+    const int64_t cnt = static_cast<int64_t>(g.items.size());
+    d->rg.push_back({g.rank, cnt, off, dpat(g.pat), g.pat.is_contiguous(), g.pat.start});
+    off += cnt;
+  }
+  d->n_leafside = off;
+  off = 0;
+  for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size(); ++gi) {
+    const auto& g = leaf_groups_[gi];
+    const int64_t cnt = static_cast<int64_t>(g.items.size());
+    d->lg.push_back({g.rank, cnt, off, dpat(g.pat), g.pat.is_contiguous(), g.pat.start});
+    off += cnt;
+  }
+  d->n_rootside = off;
+  SFG_REQUIRE(d->n_leafside <= kI32Max && d->n_rootside <= kI32Max,
+              "remote edge count exceeds the int32 range of device plans");
+
+  // Does any root receive more than one remote contribution?
+  if (d->lg.size() > 0) {
+    std::vector<uint8_t> seen(static_cast<size_t>(nroots_), 0);
+    for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size() && !d->remote_root_dups; ++gi)
+      for (int64_t r : leaf_groups_[gi].items) {
+        if (seen[static_cast<size_t>(r)]) {
+          d->remote_root_dups = true;
+          break;
+        }
+        seen[static_cast<size_t>(r)] = 1;
+      }
+  }
+  d->built = true;
+  dev_ = std::move(d);
+  return *dev_;
+}
+
+// Root-sorted CSR of every contribution in the reference's fold order:
+// self edges (ascending leaf index), then remote groups in ascending rank,
+// each in wire order (ascending leaf index on the leaf rank).
+void StarForest::ensure_csr() {
+  DevPlan& d = dev();
+  if (d.csr_built) return;
+  comm_->bind_device();
+  const bool self = d.has_self;
+  std::vector<int32_t> cnt_self(static_cast<size_t>(nroots_), 0), cnt_all(static_cast<size_t>(nroots_), 0);
+  if (self)
+    for (int64_t r : leaf_groups_.front().items) {
+      ++cnt_self[static_cast<size_t>(r)];
+      ++cnt_all[static_cast<size_t>(r)];
+    }
+  for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size(); ++gi)
+    for (int64_t r : leaf_groups_[gi].items) ++cnt_all[static_cast<size_t>(r)];
+
+  std::vector<int32_t> roots, offs, split;
+  std::vector<int64_t> cursor(static_cast<size_t>(nroots_), -1);
+  int64_t total = 0;
+  for (int64_t r = 0; r < nroots_; ++r) {
+    const int32_t c = cnt_all[static_cast<size_t>(r)];
+    if (c == 0) continue;
+    cursor[static_cast<size_t>(r)] = total;
+    roots.push_back(static_cast<int32_t>(r));
+    offs.push_back(static_cast<int32_t>(total));
+    split.push_back(static_cast<int32_t>(total + cnt_self[static_cast<size_t>(r)]));
+    total += c;
+    SFG_REQUIRE(total <= kI32Max, "CSR exceeds the int32 range of device plans");
+  }
+  offs.push_back(static_cast<int32_t>(total));
+  std::vector<int32_t> ent(static_cast<size_t>(total));
+  if (self) {
+    const auto& lg = leaf_groups_.front();
+    const auto& rg = root_groups_.front();
+    for (size_t i = 0; i < lg.items.size(); ++i) {
+      const int64_t leaf = leaf_index(rg.items[i]);
+      SFG_REQUIRE(leaf <= kI32Max, "leaf index exceeds the int32 range of device plans");
+      ent[static_cast<size_t>(cursor[static_cast<size_t>(lg.items[i])]++)] = static_cast<int32_t>(leaf);
+    }
+  }
+  size_t k = 0;
+  for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size(); ++gi, ++k) {
+    const auto& g = leaf_groups_[gi];
+    const int64_t base = d.lg[k].stage_off;
+    for (size_t i = 0; i < g.items.size(); ++i)
+      ent[static_cast<size_t>(cursor[static_cast<size_t>(g.items[i])]++)] =
+          static_cast<int32_t>(-(base + static_cast<int64_t>(i)) - 1);
+  }
+  d.csr_n = static_cast<int64_t>(roots.size());
+  const size_t bytes = (roots.size() + offs.size() + split.size() + ent.size()) * sizeof(int32_t);
+  if (bytes) {
+    SFG_CUDA(cudaMalloc(&d.csr_blob, bytes));
+    auto* p = static_cast<int32_t*>(d.csr_blob);
+    auto put = [&](const std::vector<int32_t>& v, int32_t*& dst) {
+      dst = p;
+      if (!v.empty()) SFG_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+      p += v.size();
+    };
+    put(roots, d.csr_roots);
+    put(offs, d.csr_off);
+    put(split, d.csr_split);
+    put(ent, d.csr_ent);
+  }
+  d.csr_built = true;
+}
+
+Staging* StarForest::acquire_staging(size_t ub, cudaStream_t stream) {
+  DevPlan& d = dev();
+  for (auto& s : staging_) {
+    if (s->in_use || s->unit_bytes != ub) continue;
+    s->in_use = true;
+    if (s->released_recorded) SFG_CUDA(cudaStreamWaitEvent(stream, s->released, 0));
+    return s.get();
+  }
+  auto s = std::make_unique<Staging>();
+  s->unit_bytes = ub;
+  s->leaf_bytes = static_cast<size_t>(d.n_leafside) * ub;
+  s->root_bytes = static_cast<size_t>(d.n_rootside) * ub;
+  if (s->leaf_bytes) SFG_CUDA(cudaMalloc(&s->leaf_stage, s->leaf_bytes));
+  if (s->root_bytes) SFG_CUDA(cudaMalloc(&s->root_stage, s->root_bytes));
+  SFG_CUDA(cudaMalloc(&s->digest, sizeof(unsigned long long)));
+  SFG_CUDA(cudaEventCreateWithFlags(&s->released, cudaEventDisableTiming));
+  s->in_use = true;
+  staging_.push_back(std::move(s));
+  return staging_.back().get();
+}
+
+void StarForest::release_staging(Staging* s, cudaStream_t stream) {
+  SFG_CUDA(cudaEventRecord(s->released, stream));
+  s->released_recorded = true;
+  s->in_use = false;
+}
+
+}  // namespace sfg
