@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Benchmark of the star-forest Bcast+Reduce path on B200 (BASELINE config 2).
+
+Workload: the PETSc DMDA global->local star forest of a 512^3 float64 grid
+with a 7-point (star) stencil, block-partitioned over the N ranks of the run
+(1x1x1, 1x1x2, 1x2x2, 2x2x2): every rank's interior 3-D subblock (self
+edges, Affine3D pattern) plus ghost faces from its neighbours (remote edges,
+NCCL). One step = Bcast(REPLACE) global->local + Reduce(SUM) local->global
+through the C ABI, all ranks, stream-ordered. Total grid fixed as N grows
+("strong" scaling). Arrays are 1+ GB per rank, far above the 126 MB L2, so no
+flush is needed between iterations.
+
+value   = algorithmic bytes of all ranks' launches per step / max-over-ranks
+          device time per step (GB/s); ms_per_step, us_per_op beside it.
+e2e     = same metric through the public API with the root vector copied in
+          from pinned host memory and read back every step.
+roofline: dominant kernel's algorithmic bytes per launch / its CUDA-event
+          duration on the launching stream, against MEASURED_PEAKS.json.
+cpu_baseline: the unmodified reference library (oracle/_ref) timed on the
+          box's host on a bounded slab of the same workload.
+
+`--impl reference` runs the reference arm instead (rank 0 only under torchrun).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SF Bcast+Reduce GB/s and µs/op on 3D 7-pt halo SF at 1/2/4/8 B200"
+HBM_FALLBACK = 6650.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--N", type=int, default=512)
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--sample-nz", type=int, default=64, help="reference sample: z planes per rank")
+    p.add_argument("--sample-steps", type=int, default=10)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id = gpu_id
+        self.lines: list[str] = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu_id}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def g2l_step_bytes(geo) -> float:
+    """Algorithmic bytes per Bcast(REPLACE)+Reduce(SUM) of one rank, f64:
+    interior self edges 8+8 (bcast) + 8+16 (reduce) per point; ghost faces
+    are packed/unpacked from HBM on both ends (counted by the library)."""
+    return 40.0 * geo.n_owned
+
+
+# ------------------------------------------------------------- reference arm
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import ref
+    from paper_2102_13018_b200 import graphs
+
+    P = world
+    sample = (args.N, args.N, min(args.N, args.sample_nz * P))
+    line = {"impl": "reference", "metric": METRIC, "unit": "GB/s", "higher_is_better": True,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup}
+    if not ref.available():
+        line["unavailable"] = "oracle/_ref/libsfref.so not built (needs /root/reference at build time)"
+        print(json.dumps(line))
+        return
+    specs = [graphs.g2l_halo(sample, P, r) for r in range(P)]
+    geo = [graphs.G2L(sample, P, r) for r in range(P)]
+    steps = max(1, min(args.steps, args.sample_steps))
+    t = ref.time_bcast_reduce(specs, steps, 1)
+    byts = sum(g2l_step_bytes(g) for g in geo)
+    gbs = byts / (t["us_per_step"] * 1e-6) / 1e9
+    cores = os.cpu_count()
+    line.update({
+        "value": gbs, "ms_per_step": t["us_per_step"] / 1e3,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "g2l_halo_7pt", "grid": [args.N] * 3, "parallelism": f"sf{P}",
+                   "sample_grid": list(sample), "setup_s": t["setup_s"],
+                   "bcast_us": t["bcast_us"], "reduce_us": t["reduce_us"]},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": P, "kind": "reference",
+                         "sample": f"G2L {sample[0]}x{sample[1]}x{sample[2]} over {P} rank thread(s), "
+                                   f"{steps} timed steps; host has {cores} cores"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    })
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------ our arm
+def cpu_baseline(args):
+    from oracle import ref
+    from paper_2102_13018_b200 import graphs
+
+    if not ref.available():
+        return None
+    sample = (args.N, args.N, min(args.N, args.sample_nz))
+    spec = [graphs.g2l_halo(sample, 1, 0)]
+    geo = graphs.G2L(sample, 1, 0)
+    t = ref.time_bcast_reduce(spec, args.sample_steps, 1)
+    gbs = g2l_step_bytes(geo) / (t["us_per_step"] * 1e-6) / 1e9
+    return {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "reference",
+            "sample": f"G2L {sample[0]}x{sample[1]}x{sample[2]} slab, 1 rank thread, "
+                      f"{args.sample_steps} timed Bcast+Reduce steps (reference is single-threaded "
+                      f"per rank); SetUp {t['setup_s']:.2f} s",
+            "ms_per_step": t["us_per_step"] / 1e3}
+
+
+def ours(args, rank, world, local):
+    import torch
+
+    from paper_2102_13018_b200 import graphs, sf
+
+    torch.cuda.set_device(local)
+    dev = local
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [sf.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = sf.Comm(world, rank, dev, sf.CommConfig(nranks=world, backend="nccl"), nccl_id=obj[0])
+    else:
+        dist = None
+        comm = sf.Comm(1, 0, dev, sf.CommConfig(nranks=1, backend="threads"))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def allreduce(x: float, op: str) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return float(t.item())
+
+    t0 = time.perf_counter()
+    spec = graphs.g2l_halo(args.N, world, rank)
+    geo = graphs.G2L(args.N, world, rank)
+    gen_s = time.perf_counter() - t0
+    f = sf.StarForest(comm)
+    f.set_graph_spec(spec)
+    t0 = time.perf_counter()
+    f.setup()
+    setup_s = time.perf_counter() - t0
+    del spec
+
+    unit = sf.Unit(sf.Kind.float64)
+    root = (1.0 + (torch.arange(geo.n_owned, device="cuda", dtype=torch.float64) % 97) * 1e-3)
+    leaf = torch.zeros(geo.n_local, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.Stream()
+
+    def step():
+        h = sf.bcast_begin(f, unit, root, leaf, sf.ReduceOp.replace, stream)
+        sf.bcast_end(h)
+        h = sf.reduce_begin(f, unit, leaf, root, sf.ReduceOp.sum, stream)
+        sf.reduce_end(h)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(3, args.warmup)):
+            step()
+    torch.cuda.synchronize()
+    barrier()
+
+    sampler = None
+    if rank == 0:
+        uuid = str(torch.cuda.get_device_properties(dev).uuid)
+        sampler = ClockSampler(uuid if uuid.startswith("GPU-") else f"GPU-{uuid}")
+        sampler.start()
+        time.sleep(0.15)
+    c0 = sf.counters()
+    sf.timing_enable(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    sf.timing_enable(False)
+    clocks = sampler.stop() if sampler else None
+    c1 = sf.counters()
+    timing = sf.timing_collect()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms_max = allreduce(ms, "max")
+    launches = sum(v["launches"] for v in timing.values())
+    bytes_step = sum(v["bytes"] for v in timing.values()) / args.steps
+    bytes_all = allreduce(bytes_step, "sum")
+    value = bytes_all / (ms_max * 1e-3) / 1e9
+    kl = allreduce(float(c1["kernel_launches"] - c0["kernel_launches"]), "sum")
+    net_bytes = allreduce(float(c1["bytes_sent"] - c0["bytes_sent"]) / args.steps, "sum")
+
+    # roofline of the dominant kernel (largest device time in the region)
+    peak, peak_kind = peaks()
+    dom_tag, dom = max(timing.items(), key=lambda kv: kv[1]["total_ms"])
+    per_launch_bytes = dom["bytes"] / dom["launches"]
+    per_launch_ms = dom["total_ms"] / dom["launches"]
+    achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"P{world}", {}).get(dom_tag)
+        except Exception:
+            traffic = None
+    share = dom["total_ms"] / max(1e-9, ev0.elapsed_time(ev1))
+
+    # end-to-end: root vector from pinned host memory in, result back out
+    e2e = None
+    if not args.no_e2e:
+        host_in = root.cpu().pin_memory()
+        host_out = torch.empty_like(host_in).pin_memory()
+        with torch.cuda.stream(stream):
+            root.copy_(host_in, non_blocking=True)
+            step()
+            host_out.copy_(root, non_blocking=True)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(args.e2e_steps):
+                root.copy_(host_in, non_blocking=True)
+                step()
+                host_out.copy_(root, non_blocking=True)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = allreduce(e0.elapsed_time(e1) / args.e2e_steps, "max")
+        hb = allreduce(float(geo.n_owned * 8), "sum")
+        e2e = {"value": bytes_all / (ems * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": int(hb), "d2h_bytes_per_step": int(hb)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(args)
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "error": str(e)}
+
+    if rank == 0:
+        px, py, pz = graphs.proc_grid(world)
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "g2l_halo_7pt (BASELINE config 2: DMDA global->local SF, "
+                                   "Bcast REPLACE + Reduce SUM)",
+                       "grid": [args.N] * 3, "decomposition": [px, py, pz],
+                       "parallelism": f"sf{world}", "us_per_op": ms_max * 1e3 / 2,
+                       "bytes_per_step": bytes_all, "nvlink_bytes_per_step": net_bytes,
+                       "l2": "inputs > L2: 1.07 GB roots + 1.09 GB leaves per rank at N=1",
+                       "setup_s": setup_s, "graph_gen_s": gen_s, "deterministic": True,
+                       "transport": "nccl" if world > 1 else "none (self edges only)"},
+            "gpu_launches": int(kl),
+            "roofline": {"bound": "hbm", "kernel": dom_tag, "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "bytes_per_launch": per_launch_bytes,
+                         "us_per_launch": per_launch_ms * 1e3, "share_of_step": share},
+            "kernels": {k: {"launches": v["launches"], "us_per_launch": 1e3 * v["total_ms"] / v["launches"],
+                            "GBps": v["bytes"] / (v["total_ms"] * 1e-3) / 1e9 if v["total_ms"] else None}
+                        for k, v in timing.items()},
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+    ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

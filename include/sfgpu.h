@@ -158,6 +158,19 @@ int sfg_pattern_analyze(const int64_t* idx, int64_t n, int infer_affine, int64_t
 int sfg_counters_get(sfg_counters* out);
 int sfg_counters_reset(void);
 
+/* Per-launch device timing: when enabled, CUDA events are recorded on the
+ * launching stream around every kernel of the library; collect() waits for
+ * them and aggregates per launch tag ("bcast_begin", "reduce_end", ...),
+ * with the launch's algorithmic bytes (compulsory HBM traffic). */
+typedef struct sfg_timing {
+  char tag[32];
+  uint64_t launches;
+  double total_ms;
+  double bytes;
+} sfg_timing;
+int sfg_timing_enable(int on);
+int sfg_timing_collect(sfg_timing* out, int cap, int* n);
+
 #ifdef __cplusplus
 }
 #endif

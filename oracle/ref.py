@@ -38,6 +38,8 @@ def _load():
         lib.sfref_two_sided.argtypes = G + [V, V]
         lib.sfref_time_bcast_reduce.argtypes = G + [I, I, V]
         lib.sfref_last_error.restype = C.c_char_p
+        lib.sfref_rng.argtypes = [C.c_uint64, I64, V, C.c_uint64, V]
+        lib.sfref_random_graph.argtypes = [C.c_uint64, I, I64, V, I64]
         _lib = lib
     return _lib
 
@@ -124,3 +126,28 @@ def time_bcast_reduce(specs, steps: int, warmup: int) -> dict:
         raise RuntimeError(_load().sfref_last_error().decode())
     return {"setup_s": float(out[0]), "us_per_step": float(out[1]), "bcast_us": float(out[2]),
             "reduce_us": float(out[3])}
+
+
+def rng(seed: int, n: int, salt: int = 0):
+    out = np.zeros(n, np.uint64)
+    mixed = np.zeros(1, np.uint64)
+    _load().sfref_rng(seed, n, out.ctypes.data, salt, mixed.ctypes.data)
+    return out, int(mixed[0])
+
+
+def random_graph(seed: int, nranks: int, max_vertices: int):
+    """The reference's random_graph_specs as (nroots, nleaves, local|None, ranks, offs) per rank."""
+    cap = nranks * (3 + 4 * (max_vertices + 1)) + 16
+    out = np.zeros(cap, np.int64)
+    n = _load().sfref_random_graph(seed, nranks, max_vertices, out.ctypes.data, cap)
+    if n < 0:
+        raise RuntimeError(_load().sfref_last_error().decode())
+    res, p = [], 0
+    for _ in range(nranks):
+        nroots, nleaves, has_local = int(out[p]), int(out[p + 1]), int(out[p + 2]); p += 3
+        local = None
+        if has_local:
+            local = out[p:p + nleaves].copy(); p += nleaves
+        pairs = out[p:p + 2 * nleaves].reshape(-1, 2); p += 2 * nleaves
+        res.append((nroots, nleaves, local, pairs[:, 0].astype(np.int32).copy(), pairs[:, 1].copy()))
+    return res

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "sf/harness.hpp"
+#include "sf/rng.hpp"
 #include "sf/ops.hpp"
 #include "sf/starforest.hpp"
 
@@ -176,6 +177,40 @@ int sfref_time_bcast_reduce(int nranks, const int64_t* nroots, const int64_t* nl
   } catch (const std::exception& e) {
     g_err = e.what();
     return 1;
+  }
+}
+
+// The reference's splitmix64 stream and mix_seed (rng.hpp:14-51), to pin the
+// Python port used by the generators.
+int sfref_rng(uint64_t seed, int64_t n, uint64_t* out, uint64_t salt, uint64_t* mixed) {
+  sf::Rng r(seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = r.next();
+  *mixed = sf::mix_seed(seed, salt);
+  return 0;
+}
+
+// random_graph_specs (harness.cpp:148-193) flattened per rank as
+// [nroots, nleaves, has_local, local[nleaves] if has_local, (rank, off)*nleaves].
+int sfref_random_graph(uint64_t seed, int nranks, int64_t maxv, int64_t* out, int64_t cap) {
+  try {
+    auto specs = sf::random_graph_specs(seed, nranks, maxv);
+    std::vector<int64_t> v;
+    for (const auto& s : specs) {
+      v.push_back(s.nroots);
+      v.push_back(s.nleaves);
+      v.push_back(s.local ? 1 : 0);
+      if (s.local) v.insert(v.end(), s.local->begin(), s.local->end());
+      for (const auto& r : s.remote) {
+        v.push_back(r.rank);
+        v.push_back(r.offset);
+      }
+    }
+    if (static_cast<int64_t>(v.size()) > cap) throw sf::Error("random_graph: output too small");
+    std::memcpy(out, v.data(), v.size() * sizeof(int64_t));
+    return static_cast<int>(v.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
   }
 }
 

@@ -103,7 +103,14 @@ _SIGS = {
                                       C.POINTER(sfg_pattern)]),
     "sfg_counters_get": (C.c_int, [C.POINTER(sfg_counters)]),
     "sfg_counters_reset": (C.c_int, []),
+    "sfg_timing_enable": (C.c_int, [C.c_int]),
+    "sfg_timing_collect": (C.c_int, [_V, C.c_int, C.POINTER(C.c_int)]),
 }
+
+
+class sfg_timing(C.Structure):
+    _fields_ = [("tag", C.c_char * 32), ("launches", C.c_uint64), ("total_ms", C.c_double),
+                ("bytes", C.c_double)]
 
 EXPORTED = tuple(_SIGS)
 

@@ -355,4 +355,25 @@ int sfg_counters_reset(void) {
   return guard([&] { sfg::counters().reset(); });
 }
 
+int sfg_timing_enable(int on) {
+  return guard([&] { sfg::timing_enable(on != 0); });
+}
+
+int sfg_timing_collect(sfg_timing* out, int cap, int* n) {
+  return guard([&] {
+    auto recs = sfg::timing_collect();
+    int k = 0;
+    for (const auto& r : recs) {
+      if (k >= cap) break;
+      std::memset(out[k].tag, 0, sizeof(out[k].tag));
+      std::strncpy(out[k].tag, r.tag.c_str(), sizeof(out[k].tag) - 1);
+      out[k].launches = r.launches;
+      out[k].total_ms = r.total_ms;
+      out[k].bytes = r.bytes;
+      ++k;
+    }
+    *n = k;
+  });
+}
+
 }  // extern "C"

@@ -83,9 +83,10 @@ struct Launch {
   LaunchParams p{};
   bool any_op = false;
 
-  void add(const DSeg& s) {
+  void add(const DSeg& s, int64_t entries = 0) {
     if (s.n <= 0) return;
     SFG_REQUIRE(p.nseg < kMaxSegs, "too many segments in one launch");
+    csr_entries[p.nseg] = entries;
     p.seg[p.nseg++] = s;
     if (!s.replace) any_op = true;
   }
@@ -124,11 +125,50 @@ struct Launch {
       }
       p.bl = u.blocklen;
     }
+    const bool timed = timing_enabled();
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timed) {
+      e0 = timing_event();
+      e1 = timing_event();
+      SFG_CUDA(cudaEventRecord(e0, st));
+    }
     const int launched = launch_segments(p, t, kop, st);
     SFG_REQUIRE(launched >= 0, "no kernel instantiation for this unit/op combination");
     SFG_CUDA(cudaGetLastError());
     counters().kernel_launches += static_cast<uint64_t>(launched);
+    if (timed) {
+      SFG_CUDA(cudaEventRecord(e1, st));
+      timing_record(tag, e0, e1, algorithmic_bytes(u));
+    }
   }
+
+  // Compulsory bytes of this launch: every element read once and written
+  // once, destination reads for reductions, int32 indices of Indexed
+  // patterns; affine/contiguous patterns cost no index traffic.
+  double algorithmic_bytes(const Unit& u) const {
+    const double ub = static_cast<double>(u.bytes());
+    double b = 0;
+    for (int s = 0; s < p.nseg; ++s) {
+      const DSeg& g = p.seg[s];
+      const double n = static_cast<double>(g.n);
+      const double idx = 4.0 * n * ((g.src.kind == PAT_INDEXED) + (g.dst.kind == PAT_INDEXED));
+      switch (g.type) {
+        case SEG_PAIR:
+        case SEG_PAIR_ATOMIC: b += n * ub * (g.replace ? 2.0 : 3.0) + idx; break;
+        case SEG_ATOMIC_FETCH: b += n * ub * 4.0 + idx; break;
+        case SEG_CSR_FOLD:
+        case SEG_CSR_FETCH: {
+          const double e = static_cast<double>(csr_entries[s]);
+          b += n * ub * 2.0 + e * ub * (g.type == SEG_CSR_FETCH ? 2.0 : 1.0) + 4.0 * e + 12.0 * n;
+          break;
+        }
+      }
+    }
+    return b;
+  }
+
+  const char* tag = "kernel";
+  int64_t csr_entries[kMaxSegs] = {};
 };
 
 void set_bufs(Launch& L, const OpHandle& h, void* root, void* leaf, const void* src_ro) {
@@ -188,12 +228,22 @@ void end_common(OpHandle& h) {
 }
 
 // ---------------------------------------------------------- root -> leaf
+const char* tag_of(const OpHandle& h, bool begin) {
+  static const char* names[5][2] = {{"bcast_end", "bcast_begin"},
+                                    {"reduce_end", "reduce_begin"},
+                                    {"fetch_end", "fetch_begin"},
+                                    {"gather_end", "gather_begin"},
+                                    {"scatter_end", "scatter_begin"}};
+  return names[static_cast<int>(h.kind)][begin ? 1 : 0];
+}
+
 void begin_root_to_leaf(OpHandle& h) {
   StarForest& sf = *h.sf;
   DevPlan& d = sf.dev();
   const size_t ub = h.unit.bytes();
   const bool replace = h.op == ReduceOp::replace;
   Launch L;
+  L.tag = tag_of(h, true);
   set_bufs(L, h, const_cast<void*>(h.src), h.dst, h.src);
 
   std::vector<XferOp> sends;
@@ -231,6 +281,7 @@ void end_root_to_leaf(OpHandle& h) {
   const bool replace = h.op == ReduceOp::replace;
   if (!h.recvs.empty()) sf.comm().transport().finish(data_tag(h.opid), h.recvs, h.stream);
   Launch L;
+  L.tag = tag_of(h, false);
   set_bufs(L, h, const_cast<void*>(h.src), h.dst, h.src);
   for (size_t k = 0; k < d.rg.size(); ++k) {
     if (h.zero_copy_recv[k]) continue;
@@ -249,6 +300,7 @@ void begin_leaf_to_root(OpHandle& h) {
   const bool replace = h.op == ReduceOp::replace;
   const bool det = sf.comm().config().deterministic;
   Launch L;
+  L.tag = tag_of(h, true);
   set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
 
   std::vector<XferOp> sends;
@@ -268,7 +320,7 @@ void begin_leaf_to_root(OpHandle& h) {
       L.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, replace));
     } else if (det) {
       sf.ensure_csr();
-      L.add(csr_seg(d, CsrRange::self_only, SEG_CSR_FOLD));
+      L.add(csr_seg(d, CsrRange::self_only, SEG_CSR_FOLD), d.csr_self_entries);
     } else {
       L.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, false, true));
     }
@@ -297,6 +349,7 @@ void end_leaf_to_root(OpHandle& h) {
   const bool det = sf.comm().config().deterministic;
   if (!h.recvs.empty()) sf.comm().transport().finish(data_tag(h.opid), h.recvs, h.stream);
   Launch L;
+  L.tag = tag_of(h, false);
   set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
   if (!d.lg.empty()) {
     if (replace || !d.remote_root_dups) {
@@ -310,7 +363,7 @@ void end_leaf_to_root(OpHandle& h) {
     } else if (det) {
       // Ascending-rank fold of every remote contribution (ops.cpp:372-376).
       sf.ensure_csr();
-      L.add(csr_seg(d, CsrRange::remote_only, SEG_CSR_FOLD));
+      L.add(csr_seg(d, CsrRange::remote_only, SEG_CSR_FOLD), d.csr_remote_entries);
       counters().unpack_copies += d.lg.size();
     } else {
       for (const auto& g : d.lg) {
@@ -328,6 +381,7 @@ void begin_fetch(OpHandle& h) {
   DevPlan& d = sf.dev();
   const size_t ub = h.unit.bytes();
   Launch L;
+  L.tag = "fetch_begin";
   set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
   std::vector<XferOp> sends;
   for (const auto& g : d.rg) {
@@ -362,10 +416,11 @@ void end_fetch(OpHandle& h) {
   // Root side: serialize every contribution per root.
   {
     Launch L;
+    L.tag = "fetch_end";
     set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
     if (det) {
       sf.ensure_csr();
-      L.add(csr_seg(d, CsrRange::all, SEG_CSR_FETCH));
+      L.add(csr_seg(d, CsrRange::all, SEG_CSR_FETCH), d.csr_self_entries + d.csr_remote_entries);
     } else {
       if (d.has_self) {
         DSeg s = pair_seg(d.self_leaf, BUF_SRC_RO, d.self_root, BUF_ROOT, d.n_self, false);
@@ -401,6 +456,7 @@ void end_fetch(OpHandle& h) {
     sf.comm().transport().finish(reply_tag(h.opid), h.reply_recvs, h.stream);
   }
   Launch U;
+  U.tag = "fetch_end_replies";
   set_bufs(U, h, h.dst, const_cast<void*>(h.src), h.src);
   for (size_t k = 0; k < d.rg.size(); ++k) {
     if (h.zero_copy_recv[k]) continue;

@@ -10,6 +10,7 @@
 // back to Indexed, never mis-address.
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <sstream>
 
 #include "sfg.hpp"
@@ -73,8 +74,8 @@ void nccl_check(ncclResult_t r, const char* what, const char* file, int line) {
 // /root/reference/proj/include/sf/unit.hpp:72-82 (same messages)
 void check_unit_op(const Unit& u, ReduceOp op) {
   SFG_REQUIRE(u.blocklen >= 1, "unit blocklen must be >= 1");
-  SFG_REQUIRE(static_cast<int>(u.kind) >= 0 && static_cast<int>(u.kind) <= 3, "unknown unit kind");
-  SFG_REQUIRE(static_cast<int>(op) >= 0 && static_cast<int>(op) <= 8, "unknown reduction");
+  SFG_REQUIRE(static_cast<int>(u.kind) <= 3, "unknown unit kind");
+  SFG_REQUIRE(static_cast<int>(op) <= 8, "unknown reduction");
   if (op == ReduceOp::replace) return;
   SFG_REQUIRE(u.kind != Kind::bytes, std::string("reduction '") + op_name(op) +
                                          "' requires a non-opaque unit kind");
@@ -100,6 +101,78 @@ void Counters::reset() {
 Counters& counters() {
   static Counters c;
   return c;
+}
+
+// ------------------------------------------------------------------- timing
+
+namespace {
+struct TimingState {
+  std::mutex mu;
+  bool on = false;
+  struct Pending {
+    std::string tag;
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> pool;
+};
+TimingState& ts() {
+  static TimingState t;
+  return t;
+}
+}  // namespace
+
+void timing_enable(bool on) {
+  std::lock_guard<std::mutex> lk(ts().mu);
+  ts().on = on;
+}
+
+bool timing_enabled() { return ts().on; }
+
+cudaEvent_t timing_event() {
+  {
+    std::lock_guard<std::mutex> lk(ts().mu);
+    if (!ts().pool.empty()) {
+      cudaEvent_t e = ts().pool.back();
+      ts().pool.pop_back();
+      return e;
+    }
+  }
+  cudaEvent_t e;
+  SFG_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void timing_record(const char* tag, cudaEvent_t a, cudaEvent_t b, double bytes) {
+  std::lock_guard<std::mutex> lk(ts().mu);
+  ts().pending.push_back({tag, a, b, bytes});
+}
+
+std::vector<TimingRec> timing_collect() {
+  std::vector<TimingState::Pending> pend;
+  {
+    std::lock_guard<std::mutex> lk(ts().mu);
+    pend.swap(ts().pending);
+  }
+  std::vector<TimingRec> out;
+  for (auto& p : pend) {
+    SFG_CUDA(cudaEventSynchronize(p.b));
+    float ms = 0.f;
+    SFG_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    auto it = std::find_if(out.begin(), out.end(), [&](const TimingRec& r) { return r.tag == p.tag; });
+    if (it == out.end()) {
+      out.push_back(TimingRec{p.tag, 0, 0.0, 0.0});
+      it = out.end() - 1;
+    }
+    it->launches++;
+    it->total_ms += ms;
+    it->bytes += p.bytes;
+    std::lock_guard<std::mutex> lk(ts().mu);
+    ts().pool.push_back(p.a);
+    ts().pool.push_back(p.b);
+  }
+  return out;
 }
 
 // ------------------------------------------------------------------ pattern

@@ -98,6 +98,20 @@ struct Counters {
 };
 Counters& counters();
 
+// Per-launch device timing (CUDA events recorded on the launching stream
+// around each kernel) and algorithmic bytes, for the bench's roofline.
+struct TimingRec {
+  std::string tag;
+  uint64_t launches = 0;
+  double total_ms = 0.0;
+  double bytes = 0.0;
+};
+void timing_enable(bool on);
+bool timing_enabled();
+void timing_record(const char* tag, cudaEvent_t a, cudaEvent_t b, double bytes);
+std::vector<TimingRec> timing_collect();  // synchronises the events
+cudaEvent_t timing_event();
+
 // --------------------------------------------------------------- pattern
 // Classification of an index list (/root/reference/proj/include/sf/pattern.hpp:28-102).
 // Unlike the reference (which only recognises strided subdomains when handed
@@ -281,6 +295,8 @@ struct DevPlan {
   int32_t* csr_off = nullptr;    // [csr_n + 1]
   int32_t* csr_split = nullptr;  // [csr_n]: end of self entries
   int32_t* csr_ent = nullptr;
+  int64_t csr_self_entries = 0;
+  int64_t csr_remote_entries = 0;
   ~DevPlan();
 };
 

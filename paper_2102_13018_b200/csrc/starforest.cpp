@@ -234,7 +234,6 @@ std::vector<int64_t> StarForest::compute_degrees() const {
 StarForest& StarForest::multi_sf() {
   require_state(SfState::set_up, "multi_sf");
   if (multi_) return *multi_;
-  const int me = comm_->rank();
   const int P = comm_->size();
   const auto degrees = compute_degrees();
   std::vector<int64_t> next(degrees.size());
@@ -266,7 +265,6 @@ StarForest& StarForest::multi_sf() {
       moff[static_cast<size_t>(g.items[i])] = p[i];
     }
   }
-  (void)me;
   auto m = std::make_unique<StarForest>(comm_);
   std::vector<int64_t> local;
   if (has_local_) {
@@ -415,6 +413,8 @@ void StarForest::ensure_csr() {
           static_cast<int32_t>(-(base + static_cast<int64_t>(i)) - 1);
   }
   d.csr_n = static_cast<int64_t>(roots.size());
+  d.csr_self_entries = self ? static_cast<int64_t>(leaf_groups_.front().items.size()) : 0;
+  d.csr_remote_entries = total - d.csr_self_entries;
   const size_t bytes = (roots.size() + offs.size() + split.size() + ent.size()) * sizeof(int32_t);
   if (bytes) {
     SFG_CUDA(cudaMalloc(&d.csr_blob, bytes));

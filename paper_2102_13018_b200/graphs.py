@@ -178,7 +178,9 @@ def _split(n: int, parts: int) -> list[tuple[int, int]]:
 class G2L:
     """Geometry of config 2 for one rank."""
 
-    def __init__(self, N: int, P: int, rank: int, dims: Optional[tuple[int, int, int]] = None):
+    def __init__(self, N, P: int, rank: int, dims: Optional[tuple[int, int, int]] = None):
+        """N: grid edge (int) or (NX, NY, NZ)."""
+        NX, NY, NZ = (N, N, N) if isinstance(N, int) else tuple(N)
         self.N = N
         self.P = P
         self.rank = rank
@@ -187,7 +189,7 @@ class G2L:
         self.bx = rank % self.px
         self.by = (rank // self.px) % self.py
         self.bz = rank // (self.px * self.py)
-        self.xs, self.ys, self.zs = _split(N, self.px), _split(N, self.py), _split(N, self.pz)
+        self.xs, self.ys, self.zs = _split(NX, self.px), _split(NY, self.py), _split(NZ, self.pz)
         self.nx, self.ny, self.nz = self.xs[self.bx][1], self.ys[self.by][1], self.zs[self.bz][1]
         self.X, self.Y, self.Z = self.nx + 2, self.ny + 2, self.nz + 2
 
@@ -203,7 +205,7 @@ class G2L:
         return self.X * self.Y * self.Z
 
 
-def g2l_halo(N: int, P: int, rank: int, dims=None, ghosts: bool = True,
+def g2l_halo(N, P: int, rank: int, dims=None, ghosts: bool = True,
              interior: bool = True) -> GraphSpec:
     """PETSc DMDA global->local SF, star stencil width 1, non-periodic.
 

@@ -562,6 +562,21 @@ def counters_reset() -> None:
     _check(_lib().sfg_counters_reset())
 
 
+def timing_enable(on: bool = True) -> None:
+    """Record CUDA events around every library kernel (on its launch stream)."""
+    _check(_lib().sfg_timing_enable(int(on)))
+
+
+def timing_collect() -> dict:
+    """{tag: {"launches", "total_ms", "bytes"}} for launches since the last collect."""
+    cap = 64
+    arr = (L.sfg_timing * cap)()
+    n = C.c_int()
+    _check(_lib().sfg_timing_collect(arr, cap, C.byref(n)))
+    return {arr[i].tag.decode(): {"launches": arr[i].launches, "total_ms": arr[i].total_ms,
+                                  "bytes": arr[i].bytes} for i in range(n.value)}
+
+
 # ----------------------------------------------------------------- harness
 def run_ranks(cfg: CommConfig, body: Callable[[Comm], Any], devices: Optional[Sequence[int]] = None) -> list:
     """harness.hpp:58-72: one thread per rank, results per rank; a failing or
