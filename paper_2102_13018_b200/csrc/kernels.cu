@@ -219,6 +219,56 @@ __device__ __forceinline__ void run_pair(const DSeg& s, const LaunchParams& P, i
   }
 }
 
+// Row mode: both patterns are contiguous or Affine3D and share runs of
+// `s.run` positions that are contiguous on both sides. Each warp owns 32*kItems
+// consecutive elements of the CTA's chunk; index maps are evaluated once per
+// run (not per element), then the lanes stream the run with kItems
+// independent loads in flight each.
+template <class T, int OP, bool ATOMIC>
+__device__ __forceinline__ void run_pair_rows(const DSeg& s, const LaunchParams& P, int64_t blk) {
+  const T* __restrict__ src = static_cast<const T*>(P.bufs[s.src_buf]);
+  T* dst = static_cast<T*>(P.bufs[s.dst_buf]);
+  const int64_t bl = P.bl;
+  const int64_t total = s.n * bl;
+  const ItemMap im{bl, total < (int64_t(1) << 31), P.bldiv};
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  int64_t e = blk * (kThreads * kItems) + static_cast<int64_t>(warp) * (32 * kItems);
+  const int64_t wend = min(e + 32 * kItems, total);
+  while (e < wend) {
+    int64_t pos, k;
+    im.split(e, pos, k);
+    const uint32_t r = fdiv(static_cast<uint32_t>(pos), s.rundiv);
+    const int64_t in_run = pos - static_cast<int64_t>(r) * s.run;
+    const int64_t len = min((s.run - in_run) * bl - k, wend - e);
+    const T* sp = src + pat_index(s.src, pos) * bl + k;
+    T* dp = dst + pat_index(s.dst, pos) * bl + k;
+    T v[kItems];
+    T d[kItems];
+#pragma unroll
+    for (int u = 0; u < kItems; ++u) {
+      const int64_t i = lane + 32 * u;
+      if (i < len) {
+        v[u] = sp[i];
+        if constexpr (OP != OP_REPLACE && !ATOMIC) d[u] = dp[i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kItems; ++u) {
+      const int64_t i = lane + 32 * u;
+      if (i < len) {
+        if constexpr (OP == OP_REPLACE)
+          dp[i] = v[u];
+        else if constexpr (ATOMIC)
+          (void)atomic_fetch_apply<T, OP>(dp + i, v[u]);
+        else
+          dp[i] = apply_op<T, OP>(d[u], v[u]);
+      }
+    }
+    e += len;
+  }
+}
+
 // Root-sorted fold in the reference order (self leaves ascending, then remote
 // groups ascending rank, each in ascending leaf order). Sequential per root,
 // so floating-point results are bit-identical to the CPU reference.
@@ -324,13 +374,25 @@ __global__ void __launch_bounds__(kThreads) segments_kernel(const __grid_constan
   const int64_t blk = b - P.block_start[s];
   switch (seg.type) {
     case SEG_PAIR:
-      if (seg.replace)
-        run_pair<T, OP_REPLACE, false>(seg, P, blk);
-      else
-        run_pair<T, OP, false>(seg, P, blk);
+      if (seg.run > 0) {
+        if (seg.replace)
+          run_pair_rows<T, OP_REPLACE, false>(seg, P, blk);
+        else
+          run_pair_rows<T, OP, false>(seg, P, blk);
+      } else {
+        if (seg.replace)
+          run_pair<T, OP_REPLACE, false>(seg, P, blk);
+        else
+          run_pair<T, OP, false>(seg, P, blk);
+      }
       break;
     case SEG_PAIR_ATOMIC:
-      if constexpr (OP != OP_REPLACE && sizeof(T) >= 4) run_pair<T, OP, true>(seg, P, blk);
+      if constexpr (OP != OP_REPLACE && sizeof(T) >= 4) {
+        if (seg.run > 0)
+          run_pair_rows<T, OP, true>(seg, P, blk);
+        else
+          run_pair<T, OP, true>(seg, P, blk);
+      }
       break;
     case SEG_CSR_FOLD:
       if constexpr (OP != OP_REPLACE) run_csr<T, OP>(seg, P, blk, false);

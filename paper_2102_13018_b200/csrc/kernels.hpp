@@ -75,6 +75,11 @@ struct DSeg {
   DPat src;
   DPat dst;
   int64_t n = 0;  // positions (pair) or CSR roots (csr)
+  // Pair segments whose two patterns are both contiguous/affine: positions
+  // come in runs of `run` that are contiguous on both sides (gcd of the row
+  // lengths). 0 = per-element index evaluation.
+  int64_t run = 0;
+  FastDiv rundiv;
   int32_t type = SEG_PAIR;
   int32_t replace = 0;  // 1: this segment moves data verbatim (pack)
   int32_t src_buf = 0;

@@ -36,6 +36,24 @@ DPat contig(int64_t start) {
   return p;
 }
 
+int64_t gcd64(int64_t a, int64_t b) {
+  while (b) {
+    const int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+// Length of the runs that are contiguous on both sides of a pair, or 0.
+int64_t common_run(const DPat& a, const DPat& b, int64_t n) {
+  if (a.kind == PAT_INDEXED || b.kind == PAT_INDEXED || n <= 0) return 0;
+  const int64_t ra = a.kind == PAT_CONTIG ? n : static_cast<int64_t>(a.dx.d);
+  const int64_t rb = b.kind == PAT_CONTIG ? n : static_cast<int64_t>(b.dx.d);
+  const int64_t g = gcd64(ra, rb);
+  return g >= 16 && g < (int64_t(1) << 31) ? g : 0;
+}
+
 DSeg pair_seg(const DPat& src, int sbuf, const DPat& dst, int dbuf, int64_t n, bool replace,
               bool atomic = false) {
   DSeg s;
@@ -46,6 +64,8 @@ DSeg pair_seg(const DPat& src, int sbuf, const DPat& dst, int dbuf, int64_t n, b
   s.n = n;
   s.replace = replace ? 1 : 0;
   s.type = atomic ? SEG_PAIR_ATOMIC : SEG_PAIR;
+  s.run = common_run(src, dst, n);
+  if (s.run) s.rundiv = make_fastdiv(static_cast<uint32_t>(s.run));
   return s;
 }
 
