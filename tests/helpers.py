@@ -106,3 +106,27 @@ def rank_data(specs, seed: int, dtype, blocklen: int = 1, salt0: int = 100, whic
         else:
             out.append(graphs.gen_ints(seed, salt0 + r, n, lo, hi).astype(dtype))
     return out
+
+
+def load_golden_cases(path=None):
+    """Cases of tests/golden/ref_random.npz (reference-library outputs)."""
+    import os
+
+    path = path or os.path.join(os.path.dirname(__file__), "golden", "ref_random.npz")
+    z = np.load(path)
+    cases = []
+    for ci in range(int(z["ncases"][0])):
+        k = f"c{ci}"
+        opk, dt, op, bl, nranks, seed = [str(x) for x in z[f"{k}/meta"]]
+        nranks, bl = int(nranks), int(bl)
+        specs, ins, outs = [], [], []
+        nin = sum(1 for key in z.files if key.startswith(f"{k}/r0/in"))
+        nout = sum(1 for key in z.files if key.startswith(f"{k}/r0/out"))
+        for r in range(nranks):
+            nroots, nleaves, has_local = (int(x) for x in z[f"{k}/r{r}/shape"])
+            specs.append(sf.GraphSpec(nroots, nleaves, z[f"{k}/r{r}/local"] if has_local else None,
+                                      z[f"{k}/r{r}/rr"], z[f"{k}/r{r}/ro"]))
+        ins = [[z[f"{k}/r{r}/in{i}"] for r in range(nranks)] for i in range(nin)]
+        outs = [[z[f"{k}/r{r}/out{i}"] for r in range(nranks)] for i in range(nout)]
+        cases.append((opk, dt, op, bl, specs, ins, outs))
+    return cases
