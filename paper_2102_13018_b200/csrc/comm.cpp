@@ -351,12 +351,39 @@ Comm::Comm(int nranks, int rank, int device, CommConfig cfg)
 }
 
 Comm::~Comm() {
+  if (device_ >= 0) cudaSetDevice(device_);
+  if (cstream_) cudaStreamSynchronize(cstream_);
   transport_.reset();
   ctrl_.reset();
-  if (nccl_) {
-    if (device_ >= 0) cudaSetDevice(device_);
-    ncclCommDestroy(nccl_);
+  if (nccl_) ncclCommDestroy(nccl_);
+  if (fork_ev_) cudaEventDestroy(fork_ev_);
+  if (join_ev_) cudaEventDestroy(join_ev_);
+  if (cstream_) cudaStreamDestroy(cstream_);
+}
+
+cudaStream_t Comm::comm_stream() {
+  if (!cstream_) {
+    bind_device();
+    int lo = 0, hi = 0;
+    SFG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    // Highest priority: the exchange should not queue behind a long local scatter.
+    SFG_CUDA(cudaStreamCreateWithPriority(&cstream_, cudaStreamNonBlocking, hi));
+    SFG_CUDA(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming));
+    SFG_CUDA(cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming));
   }
+  return cstream_;
+}
+
+void Comm::fork(cudaStream_t user) {
+  cudaStream_t cs = comm_stream();
+  SFG_CUDA(cudaEventRecord(fork_ev_, user));
+  SFG_CUDA(cudaStreamWaitEvent(cs, fork_ev_, 0));
+}
+
+void Comm::join(cudaStream_t user) {
+  cudaStream_t cs = comm_stream();
+  SFG_CUDA(cudaEventRecord(join_ev_, cs));
+  SFG_CUDA(cudaStreamWaitEvent(user, join_ev_, 0));
 }
 
 Transport& Comm::transport() {

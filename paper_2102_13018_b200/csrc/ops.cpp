@@ -247,24 +247,67 @@ void end_common(OpHandle& h) {
   h.stg = nullptr;
 }
 
-// ---------------------------------------------------------- root -> leaf
-const char* tag_of(const OpHandle& h, bool begin) {
-  static const char* names[5][2] = {{"bcast_end", "bcast_begin"},
-                                    {"reduce_end", "reduce_begin"},
-                                    {"fetch_end", "fetch_begin"},
-                                    {"gather_end", "gather_begin"},
-                                    {"scatter_end", "scatter_begin"}};
-  return names[static_cast<int>(h.kind)][begin ? 1 : 0];
+// ------------------------------------------------------------ exchange phases
+//
+// Begin: the comm stream forks from the caller's stream, packs every remote
+// group that is not zero-copy and posts the grouped transport call; the local
+// (self-edge) scatter runs concurrently on the caller's stream. When the local
+// segment is small it is fused into the pack launch instead (one launch, no
+// overlap to win). End: the comm stream finishes the receives, the caller's
+// stream joins it and unpacks.
+constexpr double kFuseLocalBytes = 8.0 * (1 << 20);
+
+const char* tag_of(const OpHandle& h, int phase) {  // 0 begin 1 end 2 pack 3 local
+  static const char* names[5][4] = {
+      {"bcast_begin", "bcast_end", "bcast_pack", "bcast_local"},
+      {"reduce_begin", "reduce_end", "reduce_pack", "reduce_local"},
+      {"fetch_begin", "fetch_end", "fetch_pack", "fetch_local"},
+      {"gather_begin", "gather_end", "gather_pack", "gather_local"},
+      {"scatter_begin", "scatter_end", "scatter_pack", "scatter_local"}};
+  return names[static_cast<int>(h.kind)][phase];
 }
 
+void begin_phase(OpHandle& h, Launch& pack, Launch& local, const std::vector<XferOp>& sends,
+                 const std::vector<XferOp>& recvs, uint64_t tag) {
+  Comm& c = h.sf->comm();
+  h.xfer = !sends.empty() || !recvs.empty();
+  if (!h.xfer) {
+    local.tag = tag_of(h, 0);
+    local.run(h.unit, h.op, h.stream);
+    return;
+  }
+  cudaStream_t cs = c.comm_stream();
+  c.fork(h.stream);
+  const bool fuse = local.algorithmic_bytes(h.unit) < kFuseLocalBytes;
+  if (fuse) {
+    for (int i = 0; i < local.p.nseg; ++i) pack.add(local.p.seg[i], local.csr_entries[i]);
+    pack.tag = tag_of(h, 0);
+  } else {
+    pack.tag = tag_of(h, 2);
+    local.tag = tag_of(h, 3);
+  }
+  pack.run(h.unit, h.op, cs);
+  c.transport().start(tag, sends, recvs, cs);
+  counters().transport_calls++;
+  if (!fuse) local.run(h.unit, h.op, h.stream);
+}
+
+void end_wait(OpHandle& h, uint64_t tag, const std::vector<XferOp>& recvs) {
+  if (!h.xfer) return;
+  Comm& c = h.sf->comm();
+  c.transport().finish(tag, recvs, c.comm_stream());
+  c.join(h.stream);
+}
+
+// ---------------------------------------------------------- root -> leaf
 void begin_root_to_leaf(OpHandle& h) {
   StarForest& sf = *h.sf;
   DevPlan& d = sf.dev();
   const size_t ub = h.unit.bytes();
   const bool replace = h.op == ReduceOp::replace;
-  Launch L;
-  L.tag = tag_of(h, true);
-  set_bufs(L, h, const_cast<void*>(h.src), h.dst, h.src);
+  Launch pack, local;
+  set_bufs(pack, h, const_cast<void*>(h.src), h.dst, h.src);
+  set_bufs(local, h, const_cast<void*>(h.src), h.dst, h.src);
 
   std::vector<XferOp> sends;
   for (const auto& g : d.lg) {
@@ -272,12 +315,12 @@ void begin_root_to_leaf(OpHandle& h) {
       sends.push_back({g.rank, const_cast<void*>(at(h.src, g.contig_start, ub)), static_cast<size_t>(g.n) * ub});
       counters().pack_elided++;
     } else {
-      L.add(pair_seg(g.pat, BUF_ROOT, contig(g.stage_off), BUF_ROOT_STAGE, g.n, true));
+      pack.add(pair_seg(g.pat, BUF_ROOT, contig(g.stage_off), BUF_ROOT_STAGE, g.n, true));
       sends.push_back({g.rank, at(h.stg->root_stage, g.stage_off, ub), static_cast<size_t>(g.n) * ub});
       counters().pack_copies++;
     }
   }
-  if (d.has_self) L.add(pair_seg(d.self_root, BUF_ROOT, d.self_leaf, BUF_LEAF, d.n_self, replace));
+  if (d.has_self) local.add(pair_seg(d.self_root, BUF_ROOT, d.self_leaf, BUF_LEAF, d.n_self, replace));
 
   h.recvs.clear();
   h.zero_copy_recv.clear();
@@ -288,20 +331,16 @@ void begin_root_to_leaf(OpHandle& h) {
     h.recvs.push_back({g.rank, ptr, static_cast<size_t>(g.n) * ub});
     if (zc) counters().unpack_elided++;
   }
-  L.run(h.unit, h.op, h.stream);
-  if (!sends.empty() || !h.recvs.empty()) {
-    sf.comm().transport().start(data_tag(h.opid), sends, h.recvs, h.stream);
-    counters().transport_calls++;
-  }
+  begin_phase(h, pack, local, sends, h.recvs, data_tag(h.opid));
 }
 
 void end_root_to_leaf(OpHandle& h) {
   StarForest& sf = *h.sf;
   DevPlan& d = sf.dev();
   const bool replace = h.op == ReduceOp::replace;
-  if (!h.recvs.empty()) sf.comm().transport().finish(data_tag(h.opid), h.recvs, h.stream);
+  end_wait(h, data_tag(h.opid), h.recvs);
   Launch L;
-  L.tag = tag_of(h, false);
+  L.tag = tag_of(h, 1);
   set_bufs(L, h, const_cast<void*>(h.src), h.dst, h.src);
   for (size_t k = 0; k < d.rg.size(); ++k) {
     if (h.zero_copy_recv[k]) continue;
@@ -319,9 +358,9 @@ void begin_leaf_to_root(OpHandle& h) {
   const size_t ub = h.unit.bytes();
   const bool replace = h.op == ReduceOp::replace;
   const bool det = sf.comm().config().deterministic;
-  Launch L;
-  L.tag = tag_of(h, true);
-  set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
+  Launch pack, local;
+  set_bufs(pack, h, h.dst, const_cast<void*>(h.src), h.src);
+  set_bufs(local, h, h.dst, const_cast<void*>(h.src), h.src);
 
   std::vector<XferOp> sends;
   for (const auto& g : d.rg) {
@@ -329,7 +368,7 @@ void begin_leaf_to_root(OpHandle& h) {
       sends.push_back({g.rank, const_cast<void*>(at(h.src, g.contig_start, ub)), static_cast<size_t>(g.n) * ub});
       counters().pack_elided++;
     } else {
-      L.add(pair_seg(g.pat, BUF_LEAF, contig(g.stage_off), BUF_LEAF_STAGE, g.n, true));
+      pack.add(pair_seg(g.pat, BUF_LEAF, contig(g.stage_off), BUF_LEAF_STAGE, g.n, true));
       sends.push_back({g.rank, at(h.stg->leaf_stage, g.stage_off, ub), static_cast<size_t>(g.n) * ub});
       counters().pack_copies++;
     }
@@ -337,12 +376,12 @@ void begin_leaf_to_root(OpHandle& h) {
   if (d.has_self) {
     if (replace && d.self_root_dups) counters().replace_dup_collisions++;
     if (replace || !d.self_root_dups) {
-      L.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, replace));
+      local.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, replace));
     } else if (det) {
       sf.ensure_csr();
-      L.add(csr_seg(d, CsrRange::self_only, SEG_CSR_FOLD), d.csr_self_entries);
+      local.add(csr_seg(d, CsrRange::self_only, SEG_CSR_FOLD), d.csr_self_entries);
     } else {
-      L.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, false, true));
+      local.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, false, true));
     }
   }
 
@@ -355,11 +394,7 @@ void begin_leaf_to_root(OpHandle& h) {
     h.recvs.push_back({g.rank, ptr, static_cast<size_t>(g.n) * ub});
     if (zc) counters().unpack_elided++;
   }
-  L.run(h.unit, h.op, h.stream);
-  if (!sends.empty() || !h.recvs.empty()) {
-    sf.comm().transport().start(data_tag(h.opid), sends, h.recvs, h.stream);
-    counters().transport_calls++;
-  }
+  begin_phase(h, pack, local, sends, h.recvs, data_tag(h.opid));
 }
 
 void end_leaf_to_root(OpHandle& h) {
@@ -367,9 +402,9 @@ void end_leaf_to_root(OpHandle& h) {
   DevPlan& d = sf.dev();
   const bool replace = h.op == ReduceOp::replace;
   const bool det = sf.comm().config().deterministic;
-  if (!h.recvs.empty()) sf.comm().transport().finish(data_tag(h.opid), h.recvs, h.stream);
+  end_wait(h, data_tag(h.opid), h.recvs);
   Launch L;
-  L.tag = tag_of(h, false);
+  L.tag = tag_of(h, 1);
   set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
   if (!d.lg.empty()) {
     if (replace || !d.remote_root_dups) {
@@ -400,16 +435,15 @@ void begin_fetch(OpHandle& h) {
   StarForest& sf = *h.sf;
   DevPlan& d = sf.dev();
   const size_t ub = h.unit.bytes();
-  Launch L;
-  L.tag = "fetch_begin";
-  set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
+  Launch pack, local;
+  set_bufs(pack, h, h.dst, const_cast<void*>(h.src), h.src);
   std::vector<XferOp> sends;
   for (const auto& g : d.rg) {
     if (g.contiguous) {
       sends.push_back({g.rank, const_cast<void*>(at(h.src, g.contig_start, ub)), static_cast<size_t>(g.n) * ub});
       counters().pack_elided++;
     } else {
-      L.add(pair_seg(g.pat, BUF_LEAF, contig(g.stage_off), BUF_LEAF_STAGE, g.n, true));
+      pack.add(pair_seg(g.pat, BUF_LEAF, contig(g.stage_off), BUF_LEAF_STAGE, g.n, true));
       sends.push_back({g.rank, at(h.stg->leaf_stage, g.stage_off, ub), static_cast<size_t>(g.n) * ub});
       counters().pack_copies++;
     }
@@ -417,19 +451,16 @@ void begin_fetch(OpHandle& h) {
   h.recvs.clear();
   for (const auto& g : d.lg)
     h.recvs.push_back({g.rank, at(h.stg->root_stage, g.stage_off, ub), static_cast<size_t>(g.n) * ub});
-  L.run(h.unit, ReduceOp::replace, h.stream);
-  if (!sends.empty() || !h.recvs.empty()) {
-    sf.comm().transport().start(data_tag(h.opid), sends, h.recvs, h.stream);
-    counters().transport_calls++;
-  }
+  begin_phase(h, pack, local, sends, h.recvs, data_tag(h.opid));
 }
 
 void end_fetch(OpHandle& h) {
   StarForest& sf = *h.sf;
   DevPlan& d = sf.dev();
+  Comm& c = sf.comm();
   const size_t ub = h.unit.bytes();
-  const bool det = sf.comm().config().deterministic;
-  if (!h.recvs.empty()) sf.comm().transport().finish(data_tag(h.opid), h.recvs, h.stream);
+  const bool det = c.config().deterministic;
+  end_wait(h, data_tag(h.opid), h.recvs);
   if (!d.rg.empty() && h.stg->leaf_reply == nullptr && h.stg->leaf_bytes)
     SFG_CUDA(cudaMalloc(&h.stg->leaf_reply, h.stg->leaf_bytes));
 
@@ -471,9 +502,12 @@ void end_fetch(OpHandle& h) {
     h.reply_recvs.push_back({g.rank, ptr, static_cast<size_t>(g.n) * ub});
   }
   if (!sends.empty() || !h.reply_recvs.empty()) {
-    sf.comm().transport().start(reply_tag(h.opid), sends, h.reply_recvs, h.stream);
+    cudaStream_t cs = c.comm_stream();
+    c.fork(h.stream);
+    c.transport().start(reply_tag(h.opid), sends, h.reply_recvs, cs);
     counters().transport_calls++;
-    sf.comm().transport().finish(reply_tag(h.opid), h.reply_recvs, h.stream);
+    c.transport().finish(reply_tag(h.opid), h.reply_recvs, cs);
+    c.join(h.stream);
   }
   Launch U;
   U.tag = "fetch_end_replies";

@@ -237,6 +237,13 @@ class Comm {
   uint64_t next_op_seq() { return ++op_seq_; }
   void bind_device() const;
 
+  // Every transport call of this communicator runs on one internal stream
+  // (NCCL requires a single issue order per communicator); fork/join order it
+  // against the caller's stream so exchanges overlap the local scatter.
+  cudaStream_t comm_stream();
+  void fork(cudaStream_t user);  // comm stream waits for work queued on `user`
+  void join(cudaStream_t user);  // `user` waits for work queued on the comm stream
+
   // wiring (abi.cpp)
   std::unique_ptr<ControlPlane> ctrl_;
   std::unique_ptr<Transport> transport_;
@@ -247,6 +254,8 @@ class Comm {
   int size_, rank_, device_;
   CommConfig cfg_;
   uint64_t op_seq_ = 0;
+  cudaStream_t cstream_ = nullptr;
+  cudaEvent_t fork_ev_ = nullptr, join_ev_ = nullptr;
 };
 
 std::unique_ptr<ControlPlane> make_threads_ctrl(World* w, int rank);
@@ -378,6 +387,7 @@ struct OpHandle {
   void* leafupdate = nullptr;
   uint64_t opid = 0;
   bool ended = false;
+  bool xfer = false;  // this op has transport work
   cudaStream_t stream = nullptr;
   Staging* stg = nullptr;
   std::vector<XferOp> recvs;        // phase-1 receives

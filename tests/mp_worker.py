@@ -22,10 +22,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    obj = [sf.nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=0)
     fails = []
     for deterministic in (True, False):
+        obj = [sf.nccl_unique_id() if rank == 0 else None]  # one id per communicator
+        dist.broadcast_object_list(obj, src=0)
         comm = sf.Comm(world, rank, local, sf.CommConfig(nranks=world, backend="nccl",
                                                          deterministic=deterministic), nccl_id=obj[0])
         cases = [("g2l", [graphs.g2l_halo(9, world, r) for r in range(world)])]
