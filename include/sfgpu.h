@@ -104,6 +104,21 @@ int sfg_nccl_unique_id(void* out, size_t bytes);
  * operations do not). */
 int sfg_comm_create(sfg_world world, int nranks, int rank, int device, const char* backend,
                     const void* nccl_id, const sfg_config* cfg, sfg_comm* out);
+/* Control plane supplied by the caller (e.g. torch.distributed, MPI): the
+ * host collectives SetUp and multi_sf need. Each returns 0 on success.
+ * allgather: out[r*bytes ..] = rank r's `in`. alltoallv: send holds the
+ * payloads for ranks 0..size-1 back to back (send_bytes[r] each), recv
+ * receives rank r's payload at the prefix offset of recv_bytes. */
+typedef struct sfg_ctrl_ops {
+  void* ctx;
+  int (*allgather)(void* ctx, const void* in, size_t bytes, void* out);
+  int (*alltoallv)(void* ctx, const void* send, const int64_t* send_bytes, void* recv,
+                   const int64_t* recv_bytes);
+  int (*barrier)(void* ctx);
+} sfg_ctrl_ops;
+int sfg_comm_create_ext(int nranks, int rank, int device, const char* backend,
+                        const void* nccl_id, const sfg_config* cfg, const sfg_ctrl_ops* ops,
+                        sfg_comm* out);
 int sfg_comm_destroy(sfg_comm c);
 int sfg_comm_rank(sfg_comm c, int* rank, int* size, int* device);
 

@@ -61,6 +61,17 @@ class sfg_counters(C.Structure):
         "transport_calls")]
 
 
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+ALLTOALLV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p,
+                           C.POINTER(C.c_int64))
+BARRIER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p)
+
+
+class sfg_ctrl_ops(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("allgather", ALLGATHER_FN), ("alltoallv", ALLTOALLV_FN),
+                ("barrier", BARRIER_FN)]
+
+
 # name -> (restype, argtypes); every function returns an int status
 _V = C.c_void_p
 _SIGS = {
@@ -73,6 +84,9 @@ _SIGS = {
     "sfg_nccl_unique_id": (C.c_int, [_V, C.c_size_t]),
     "sfg_comm_create": (C.c_int, [_V, C.c_int, C.c_int, C.c_int, C.c_char_p, _V,
                                   C.POINTER(sfg_config), C.POINTER(_V)]),
+    "sfg_comm_create_ext": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p, _V,
+                                      C.POINTER(sfg_config), C.POINTER(sfg_ctrl_ops),
+                                      C.POINTER(_V)]),
     "sfg_comm_destroy": (C.c_int, [_V]),
     "sfg_comm_rank": (C.c_int, [_V, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "sfg_sf_create": (C.c_int, [_V, C.POINTER(_V)]),

@@ -112,60 +112,137 @@ int sfg_nccl_unique_id(void* out, size_t bytes) {
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+// Control plane over caller-supplied callbacks (torch.distributed, MPI, ...).
+class ExtCtrl final : public sfg::ControlPlane {
+ public:
+  ExtCtrl(const sfg_ctrl_ops& ops, int rank, int size) : ops_(ops), rank_(rank), size_(size) {}
+  int rank() const override { return rank_; }
+  int size() const override { return size_; }
+  void allgather(const void* in, size_t bytes, void* out) override {
+    SFG_REQUIRE(ops_.allgather(ops_.ctx, in, bytes, out) == 0, "control plane: allgather failed");
+  }
+  std::vector<std::vector<uint8_t>> alltoallv(std::vector<std::vector<uint8_t>> send) override {
+    const size_t n = static_cast<size_t>(size_);
+    std::vector<int64_t> mine(n), all(n * n), rb(n);
+    for (size_t d = 0; d < n; ++d) mine[d] = static_cast<int64_t>(send[d].size());
+    allgather(mine.data(), n * sizeof(int64_t), all.data());
+    size_t stot = 0, rtot = 0;
+    for (size_t d = 0; d < n; ++d) stot += send[d].size();
+    for (size_t s = 0; s < n; ++s) {
+      rb[s] = all[s * n + static_cast<size_t>(rank_)];
+      rtot += static_cast<size_t>(rb[s]);
+    }
+    std::vector<uint8_t> sbuf(stot), rbuf(rtot);
+    size_t off = 0;
+    for (size_t d = 0; d < n; ++d) {
+      if (!send[d].empty()) std::memcpy(sbuf.data() + off, send[d].data(), send[d].size());
+      off += send[d].size();
+    }
+    SFG_REQUIRE(ops_.alltoallv(ops_.ctx, sbuf.data(), mine.data(), rbuf.data(), rb.data()) == 0,
+                "control plane: alltoallv failed");
+    std::vector<std::vector<uint8_t>> out(n);
+    off = 0;
+    for (size_t s = 0; s < n; ++s) {
+      out[s].assign(rbuf.begin() + static_cast<std::ptrdiff_t>(off),
+                    rbuf.begin() + static_cast<std::ptrdiff_t>(off + static_cast<size_t>(rb[s])));
+      off += static_cast<size_t>(rb[s]);
+    }
+    return out;
+  }
+  void barrier() override {
+    SFG_REQUIRE(ops_.barrier(ops_.ctx) == 0, "control plane: barrier failed");
+  }
+
+ private:
+  sfg_ctrl_ops ops_;
+  int rank_, size_;
+};
+
+sfg::CommConfig to_config(const sfg_config* cfg, const char* backend) {
+  sfg::CommConfig cc;
+  if (cfg) {
+    cc.deterministic = cfg->deterministic != 0;
+    cc.debug_checksum = cfg->debug_checksum != 0;
+    cc.force_remote = cfg->force_remote != 0;
+    cc.dense_discovery_threshold = cfg->dense_discovery_threshold;
+    cc.seed = cfg->seed;
+    cc.timeout_s = cfg->timeout_s;
+  }
+  cc.backend = backend ? backend : "threads";
+  SFG_REQUIRE(cc.backend == "threads" || cc.backend == "nccl",
+              "unknown transport backend '" + cc.backend + "' (threads | nccl)");
+  return cc;
+}
+
+sfg_comm make_comm(sfg_world world, int nranks, int rank, int device, const sfg::CommConfig& cc,
+                   const void* nccl_id, const sfg_ctrl_ops* ops) {
+  auto h = std::make_unique<sfg_comm_s>();
+  h->c = std::make_unique<sfg::Comm>(nranks, rank, device, cc);
+  sfg::Comm& c = *h->c;
+  sfg::World* w = world ? &world->w : nullptr;
+  if (w) SFG_REQUIRE(w->size() == nranks, "world size does not match nranks");
+  if (!w && cc.backend == "threads" && device >= 0) {
+    SFG_REQUIRE(nranks == 1, "the threads backend needs an in-process world for nranks > 1");
+    h->own_world = std::make_unique<sfg::World>(1, cc.timeout_s);
+    w = h->own_world.get();
+  }
+  c.world_ = w;
+  if (device >= 0) {
+    SFG_CUDA(cudaSetDevice(device));
+    SFG_CUDA(cudaFree(nullptr));  // create the context
+  }
+  if (cc.backend == "nccl") {
+    SFG_REQUIRE(device >= 0, "the nccl backend needs a device");
+    ncclUniqueId id;
+    if (nccl_id) {
+      std::memcpy(&id, nccl_id, sizeof(id));
+    } else {
+      SFG_REQUIRE(nranks == 1, "nccl backend with nranks > 1 needs a shared unique id");
+      SFG_NCCL(ncclGetUniqueId(&id));
+    }
+    SFG_NCCL(ncclCommInitRank(&c.nccl_, nranks, id, rank));
+  }
+  if (ops)
+    c.ctrl_ = std::make_unique<ExtCtrl>(*ops, rank, nranks);
+  else if (w)
+    c.ctrl_ = sfg::make_threads_ctrl(w, rank);
+  else if (nranks == 1)
+    c.ctrl_ = sfg::make_single_ctrl();
+  else {
+    SFG_REQUIRE(c.nccl_ != nullptr, "nranks > 1 without a world needs the nccl backend or control-plane callbacks");
+    c.ctrl_ = sfg::make_nccl_ctrl(c.nccl_, rank, nranks, device);
+  }
+  if (device >= 0) {
+    if (cc.backend == "nccl")
+      c.transport_ = sfg::make_nccl_transport(c.nccl_, rank, device);
+    else
+      c.transport_ = sfg::make_threads_transport(w, rank, device, cc.timeout_s);
+  }
+  return h.release();
+}
+
+}  // namespace
+
+extern "C" {
+
 int sfg_comm_create(sfg_world world, int nranks, int rank, int device, const char* backend,
                     const void* nccl_id, const sfg_config* cfg, sfg_comm* out) {
   return guard([&] {
-    sfg::CommConfig cc;
-    if (cfg) {
-      cc.deterministic = cfg->deterministic != 0;
-      cc.debug_checksum = cfg->debug_checksum != 0;
-      cc.force_remote = cfg->force_remote != 0;
-      cc.dense_discovery_threshold = cfg->dense_discovery_threshold;
-      cc.seed = cfg->seed;
-      cc.timeout_s = cfg->timeout_s;
-    }
-    cc.backend = backend ? backend : "threads";
-    SFG_REQUIRE(cc.backend == "threads" || cc.backend == "nccl",
-                "unknown transport backend '" + cc.backend + "' (threads | nccl)");
-    auto h = std::make_unique<sfg_comm_s>();
-    h->c = std::make_unique<sfg::Comm>(nranks, rank, device, cc);
-    sfg::Comm& c = *h->c;
-    sfg::World* w = world ? &world->w : nullptr;
-    if (w) SFG_REQUIRE(w->size() == nranks, "world size does not match nranks");
-    if (!w && cc.backend == "threads") {
-      SFG_REQUIRE(nranks == 1, "the threads backend needs an in-process world for nranks > 1");
-      h->own_world = std::make_unique<sfg::World>(1, cc.timeout_s);
-      w = h->own_world.get();
-    }
-    c.world_ = w;
-    if (device >= 0) {
-      SFG_CUDA(cudaSetDevice(device));
-      SFG_CUDA(cudaFree(nullptr));  // create the context
-    }
-    if (cc.backend == "nccl") {
-      SFG_REQUIRE(device >= 0, "the nccl backend needs a device");
-      ncclUniqueId id;
-      if (nccl_id) {
-        std::memcpy(&id, nccl_id, sizeof(id));
-      } else {
-        SFG_REQUIRE(nranks == 1, "nccl backend with nranks > 1 needs a shared unique id");
-        SFG_NCCL(ncclGetUniqueId(&id));
-      }
-      SFG_NCCL(ncclCommInitRank(&c.nccl_, nranks, id, rank));
-    }
-    if (w)
-      c.ctrl_ = sfg::make_threads_ctrl(w, rank);
-    else if (nranks == 1)
-      c.ctrl_ = sfg::make_single_ctrl();
-    else
-      c.ctrl_ = sfg::make_nccl_ctrl(c.nccl_, rank, nranks, device);
-    if (device >= 0) {
-      if (cc.backend == "nccl")
-        c.transport_ = sfg::make_nccl_transport(c.nccl_, rank, device);
-      else
-        c.transport_ = sfg::make_threads_transport(w, rank, device, cc.timeout_s);
-    }
-    *out = h.release();
+    *out = make_comm(world, nranks, rank, device, to_config(cfg, backend), nccl_id, nullptr);
+  });
+}
+
+int sfg_comm_create_ext(int nranks, int rank, int device, const char* backend,
+                        const void* nccl_id, const sfg_config* cfg, const sfg_ctrl_ops* ops,
+                        sfg_comm* out) {
+  return guard([&] {
+    SFG_REQUIRE(ops && ops->allgather && ops->alltoallv && ops->barrier,
+                "control-plane callbacks missing");
+    *out = make_comm(nullptr, nranks, rank, device, to_config(cfg, backend), nccl_id, ops);
   });
 }
 

@@ -163,9 +163,12 @@ class World:
         _lib().sfg_world_abort(self._h)
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib().sfg_world_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                _lib().sfg_world_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
 
 def nccl_unique_id() -> bytes:
@@ -192,6 +195,67 @@ class Comm:
         self.device = device
         self._rank, self._size = rank, nranks
 
+    @classmethod
+    def from_torch_distributed(cls, device: int = -1, config: Optional[CommConfig] = None,
+                               nccl_id: Optional[bytes] = None, group=None) -> "Comm":
+        """One rank per process; SetUp's host collectives run over an
+        initialised torch.distributed process group (gloo or nccl); the data
+        plane is the library's NCCL communicator (config.backend 'nccl',
+        nccl_id shared by the caller) or none for host-only use."""
+        import torch
+        import torch.distributed as dist
+
+        nranks, rank = dist.get_world_size(group), dist.get_rank(group)
+        tdev = torch.device("cuda", torch.cuda.current_device()) \
+            if dist.get_backend(group) == "nccl" else torch.device("cpu")
+
+        def allgather(ctx, inp, nbytes, out):
+            try:
+                t = torch.frombuffer(bytearray(C.string_at(inp, nbytes)), dtype=torch.uint8).to(tdev)
+                outs = [torch.empty(nbytes, dtype=torch.uint8, device=tdev) for _ in range(nranks)]
+                dist.all_gather(outs, t, group=group)
+                host = torch.cat(outs).cpu().numpy()
+                C.memmove(out, host.ctypes.data, nbytes * nranks)
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        def alltoallv(ctx, send, send_bytes, recv, recv_bytes):
+            try:
+                sb = [int(send_bytes[i]) for i in range(nranks)]
+                rb = [int(recv_bytes[i]) for i in range(nranks)]
+                st = torch.frombuffer(bytearray(C.string_at(send, sum(sb)) if sum(sb) else b"\0"),
+                                      dtype=torch.uint8)[:sum(sb)].to(tdev)
+                rt = torch.empty(sum(rb), dtype=torch.uint8, device=tdev)
+                dist.all_to_all_single(rt, st, output_split_sizes=rb, input_split_sizes=sb, group=group)
+                if sum(rb):
+                    host = rt.cpu().numpy()
+                    C.memmove(recv, host.ctypes.data, sum(rb))
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        def barrier(ctx):
+            try:
+                dist.barrier(group=group)
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        cfg = config or CommConfig(nranks=nranks, backend="nccl" if device >= 0 else "threads")
+        cfg.nranks = nranks
+        ops = L.sfg_ctrl_ops(None, L.ALLGATHER_FN(allgather), L.ALLTOALLV_FN(alltoallv),
+                             L.BARRIER_FN(barrier))
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+        _check(_lib().sfg_comm_create_ext(nranks, rank, device, cfg.backend.encode(), idbuf,
+                                          C.byref(cfg._c()), C.byref(ops), C.byref(h)))
+        self._h, self._world, self.config, self.device = h, None, cfg, device
+        self._rank, self._size = rank, nranks
+        self._ops = ops  # callbacks must outlive the communicator
+        return self
+
     def rank(self) -> int:
         return self._rank
 
@@ -204,7 +268,10 @@ class Comm:
             self._h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
 
 
 # --------------------------------------------------------------- star forest
@@ -287,9 +354,12 @@ class StarForest:
         self._multi: Optional[StarForest] = None
 
     def __del__(self):
-        if getattr(self, "_owned", False) and getattr(self, "_h", None):
-            _lib().sfg_sf_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_owned", False) and getattr(self, "_h", None):
+                _lib().sfg_sf_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
     # -- graph
     def set_graph(self, nroots: int, nleaves: int, local=None, remote=None, *,
@@ -447,9 +517,12 @@ class OpHandle:
         return bool(self._q()[2])
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib().sfg_handle_free(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                _lib().sfg_handle_free(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
 
 def _begin(fn, sf: StarForest, args: list, stream, keep) -> OpHandle:
