@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Secondary benchmarks for the BASELINE configurations other than the
+headline (bench.py runs config 2). One JSON line per measurement.
+
+  config 1  single rank, 4,194,304 leaves -> 1,048,576 random roots, f64:
+            Bcast REPLACE and Reduce SUM (deterministic and free-order)
+  config 3  27-point Laplacian ghost-column SF, 400^3, 8 ranks (2x2x2),
+            natural and locally permuted numbering: Bcast REPLACE, Reduce SUM
+  config 4  16,777,216 leaves -> 65,536 roots (degree 256): Reduce SUM and
+            FetchAndOp SUM, f64 and i64, deterministic and free-order
+  config 5  2-rank ping-pong (bench.cpp:24-100 shape): Bcast REPLACE +
+            Reduce REPLACE per iteration, half round trip, 8 B .. 256 MB
+
+Run on one GPU: `python bench_configs.py --config 1`; multi-GPU with
+torch.distributed.run (one process per GPU, NCCL). `--cpu` also times the
+reference library (oracle/_ref) on the same graph (rank 0, single process).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+
+
+class Ctx:
+    def __init__(self, deterministic=True):
+        import torch
+
+        from paper_2102_13018_b200 import sf
+
+        self.sf = sf
+        self.torch = torch
+        self.rank, self.world, self.local = env()
+        torch.cuda.set_device(self.local)
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+
+            if not dist.is_initialized():
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.dist = dist
+        self.stream = torch.cuda.Stream()
+        self.comms = {}
+
+    def comm(self, deterministic=True):
+        sf = self.sf
+        if deterministic in self.comms:
+            return self.comms[deterministic]
+        if self.world > 1:
+            obj = [sf.nccl_unique_id() if self.rank == 0 else None]
+            self.dist.broadcast_object_list(obj, src=0)
+            c = sf.Comm(self.world, self.rank, self.local,
+                        sf.CommConfig(nranks=self.world, backend="nccl", deterministic=deterministic),
+                        nccl_id=obj[0])
+        else:
+            c = sf.Comm(1, 0, self.local, sf.CommConfig(nranks=1, deterministic=deterministic))
+        self.comms[deterministic] = c
+        return c
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def vmax(self, x):
+        if not self.dist:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def vsum(self, x):
+        if not self.dist:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t)
+        return float(t.item())
+
+    def timed(self, fn, steps, warmup):
+        torch, sf = self.torch, self.sf
+        with torch.cuda.stream(self.stream):
+            for _ in range(warmup):
+                fn()
+        torch.cuda.synchronize()
+        self.barrier()
+        sf.timing_collect()
+        sf.timing_enable(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(self.stream):
+            e0.record(self.stream)
+            for _ in range(steps):
+                fn()
+            e1.record(self.stream)
+        torch.cuda.synchronize()
+        sf.timing_enable(False)
+        rec = sf.timing_collect()
+        ms = self.vmax(e0.elapsed_time(e1) / steps)
+        byts = self.vsum(sum(v["bytes"] for v in rec.values()) / steps)
+        self.barrier()
+        return ms, byts, rec
+
+
+def peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+def emit(ctx, d):
+    if ctx.rank == 0:
+        print(json.dumps(d), flush=True)
+
+
+def op_line(ctx, config, name, ms, byts, rec, extra=None):
+    gbs = byts / (ms * 1e-3) / 1e9
+    dom = max(rec.items(), key=lambda kv: kv[1]["total_ms"]) if rec else (None, None)
+    d = {"config": config, "op": name, "n_gpus": ctx.world, "us_per_op": ms * 1e3,
+         "GBps": gbs, "frac_hbm": gbs / peak() if ctx.world == 1 else None,
+         "kernels": {k: {"launches": v["launches"], "us": 1e3 * v["total_ms"] / v["launches"],
+                         "GBps": v["bytes"] / max(1e-12, v["total_ms"] * 1e-3) / 1e9}
+                     for k, v in rec.items()},
+         "dominant": dom[0]}
+    d.update(extra or {})
+    emit(ctx, d)
+
+
+def setup_forest(ctx, spec, deterministic=True):
+    f = ctx.sf.StarForest(ctx.comm(deterministic))
+    f.set_graph_spec(spec)
+    t0 = time.perf_counter()
+    f.setup()
+    return f, time.perf_counter() - t0
+
+
+# ------------------------------------------------------------------ config 1
+def config1(ctx, args):
+    from paper_2102_13018_b200 import graphs
+
+    torch, sf = ctx.torch, ctx.sf
+    L, R = 4194304, 1048576
+    specs = graphs.random_leaf_root(L, R, ctx.world, seed=1)
+    spec = specs[ctx.rank]
+    u = sf.Unit(sf.Kind.float64)
+    root = torch.from_numpy(graphs.gen_f64(1, 100 + ctx.rank, int(spec.nroots))).cuda()
+    leaf = torch.from_numpy(graphs.gen_f64(1, 200 + ctx.rank, spec.leaf_bound())).cuda()
+    for det in (True, False):
+        f, setup_s = setup_forest(ctx, spec, det)
+
+        def bc():
+            h = sf.bcast_begin(f, u, root, leaf, sf.ReduceOp.replace, ctx.stream)
+            sf.bcast_end(h)
+
+        def rd():
+            h = sf.reduce_begin(f, u, leaf, root, sf.ReduceOp.sum, ctx.stream)
+            sf.reduce_end(h)
+
+        for name, fn in (("bcast_replace", bc), ("reduce_sum", rd)):
+            ms, byts, rec = ctx.timed(fn, args.steps, args.warmup)
+            op_line(ctx, 1, name, ms, byts, rec, {"deterministic": det, "setup_s": setup_s,
+                                                   "L": L, "R": R, "dtype": "f64"})
+    if args.cpu and ctx.world == 1 and ctx.rank == 0:
+        from oracle import ref
+
+        if ref.available():
+            for opk, op in (("bcast", "replace"), ("reduce", "sum")):
+                t = ref.time_op(specs, opk, "float64", op, 3, 1)
+                emit(ctx, {"config": 1, "op": f"{opk}_{op}", "impl": "reference_cpu", "cores": 1,
+                           "us_per_op": t["us_per_call"], "setup_s": t["setup_s"]})
+
+
+# ------------------------------------------------------------------ config 4
+def config4(ctx, args):
+    from paper_2102_13018_b200 import graphs
+
+    torch, sf = ctx.torch, ctx.sf
+    L, R = 16777216, 65536
+    specs = graphs.random_leaf_root(L, R, ctx.world, seed=4)
+    spec = specs[ctx.rank]
+    for det in (True, False):
+        f, setup_s = setup_forest(ctx, spec, det)
+        for dt, kind in (("f64", sf.Kind.float64), ("i64", sf.Kind.int64)):
+            u = sf.Unit(kind)
+            tdt = torch.float64 if dt == "f64" else torch.int64
+            root = torch.ones(int(spec.nroots), dtype=tdt, device="cuda")
+            leaf = torch.ones(spec.leaf_bound(), dtype=tdt, device="cuda")
+            upd = torch.zeros_like(leaf)
+
+            def rd():
+                h = sf.reduce_begin(f, u, leaf, root, sf.ReduceOp.sum, ctx.stream)
+                sf.reduce_end(h)
+
+            def fo():
+                h = sf.fetch_and_op_begin(f, u, root, leaf, upd, sf.ReduceOp.sum, ctx.stream)
+                sf.fetch_and_op_end(h)
+
+            for name, fn in (("reduce_sum", rd), ("fetch_and_op_sum", fo)):
+                ms, byts, rec = ctx.timed(fn, args.steps, args.warmup)
+                op_line(ctx, 4, name, ms, byts, rec, {"deterministic": det, "dtype": dt,
+                                                       "setup_s": setup_s, "L": L, "R": R})
+    if args.cpu and ctx.world == 1 and ctx.rank == 0:
+        from oracle import ref
+
+        if ref.available():
+            for opk in ("reduce", "fetch_and_op"):
+                for dt in ("float64", "int64"):
+                    t = ref.time_op(specs, opk, dt, "sum", 3, 1)
+                    emit(ctx, {"config": 4, "op": f"{opk}_sum", "dtype": dt, "impl": "reference_cpu",
+                               "cores": 1, "us_per_op": t["us_per_call"], "setup_s": t["setup_s"]})
+
+
+# ------------------------------------------------------------------ config 5
+def config5(ctx, args):
+    from paper_2102_13018_b200 import graphs
+
+    torch, sf = ctx.torch, ctx.sf
+    assert ctx.world == 2, "config 5 needs exactly 2 ranks"
+    u = sf.Unit(sf.Kind.int64)
+    size = 8
+    rows = []
+    while size <= args.max_bytes:
+        specs = graphs.pingpong(size)
+        n = size // 8
+        f, _ = setup_forest(ctx, specs[ctx.rank])
+        root = torch.arange(n if ctx.rank == 0 else 0, dtype=torch.int64, device="cuda")
+        leaf = torch.zeros(n if ctx.rank == 1 else 0, dtype=torch.int64, device="cuda")
+        iters = 50 if size <= (1 << 20) else 10
+        dev_us, host_us = [], []
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for it in range(5 + iters):
+            torch.cuda.synchronize()
+            ctx.barrier()
+            t0 = time.perf_counter()
+            with torch.cuda.stream(ctx.stream):
+                e0.record(ctx.stream)
+                h = sf.bcast_begin(f, u, root, leaf, sf.ReduceOp.replace, ctx.stream)
+                sf.bcast_end(h)
+                h = sf.reduce_begin(f, u, leaf, root, sf.ReduceOp.replace, ctx.stream)
+                sf.reduce_end(h)
+                e1.record(ctx.stream)
+            ctx.stream.synchronize()
+            t1 = time.perf_counter()
+            if it >= 5:
+                dev_us.append(e0.elapsed_time(e1) * 1e3 / 2)
+                host_us.append((t1 - t0) * 1e6 / 2)
+        ok = True
+        if ctx.rank == 1:
+            ok = bool((leaf.cpu() == torch.arange(n)).all()) if n else True
+        dmed = ctx.vmax(statistics.median(dev_us))
+        dmin = ctx.vmax(min(dev_us))
+        hmed = ctx.vmax(statistics.median(host_us))
+        rows.append({"bytes": size, "half_rtt_us_median": dmed, "half_rtt_us_min": dmin,
+                     "host_half_rtt_us_median": hmed, "GBps": size / (dmed * 1e-6) / 1e9,
+                     "payload_ok": ok})
+        del f
+        size *= 2
+    emit(ctx, {"config": 5, "op": "pingpong_bcast+reduce_replace", "n_gpus": 2, "rows": rows})
+
+
+# ------------------------------------------------------------------ config 3
+def config3(ctx, args):
+    """8 ranks. With 8 GPUs: one process per GPU (NCCL). Otherwise: 8 thread
+    ranks in this process spread over the visible GPUs with the in-process
+    put transport (peer copies), reported as such."""
+    import threading
+
+    from paper_2102_13018_b200 import graphs
+
+    torch, sf = ctx.torch, ctx.sf
+    N = args.n3
+    for permute in (None, 3):
+        specs = [graphs.laplacian27_ghosts(N, (2, 2, 2), r, permute) for r in range(8)]
+        if ctx.world == 8:
+            f, setup_s = setup_forest(ctx, specs[ctx.rank])
+            u = sf.Unit(sf.Kind.float64)
+            root = torch.rand(int(specs[ctx.rank].nroots), dtype=torch.float64, device="cuda")
+            leaf = torch.zeros(specs[ctx.rank].leaf_bound(), dtype=torch.float64, device="cuda")
+
+            def bc():
+                h = sf.bcast_begin(f, u, root, leaf, sf.ReduceOp.replace, ctx.stream)
+                sf.bcast_end(h)
+
+            def rd():
+                h = sf.reduce_begin(f, u, leaf, root, sf.ReduceOp.sum, ctx.stream)
+                sf.reduce_end(h)
+
+            for name, fn in (("bcast_replace", bc), ("reduce_sum", rd)):
+                ms, byts, rec = ctx.timed(fn, args.steps, args.warmup)
+                op_line(ctx, 3, name, ms, byts, rec, {"permuted": permute is not None,
+                                                       "transport": "nccl", "N": N})
+            continue
+        if ctx.rank != 0:
+            continue
+        ng = torch.cuda.device_count()
+        devices = [r * ng // 8 for r in range(8)]
+        res = {}
+
+        def body(comm):
+            r = comm.rank()
+            f = sf.StarForest(comm)
+            f.set_graph_spec(specs[r])
+            f.setup()
+            u = sf.Unit(sf.Kind.float64)
+            root = torch.rand(int(specs[r].nroots), dtype=torch.float64, device="cuda")
+            leaf = torch.zeros(specs[r].leaf_bound(), dtype=torch.float64, device="cuda")
+            st = torch.cuda.Stream()
+            out = {}
+            for name, opf in (("bcast_replace", lambda: sf.bcast_end(sf.bcast_begin(
+                    f, u, root, leaf, sf.ReduceOp.replace, st))),
+                              ("reduce_sum", lambda: sf.reduce_end(sf.reduce_begin(
+                                  f, u, leaf, root, sf.ReduceOp.sum, st)))):
+                with torch.cuda.stream(st):
+                    for _ in range(3):
+                        opf()
+                st.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(st):
+                    e0.record(st)
+                    for _ in range(args.steps):
+                        opf()
+                    e1.record(st)
+                st.synchronize()
+                out[name] = e0.elapsed_time(e1) * 1e3 / args.steps
+            return out
+
+        got = sf.run_ranks(sf.CommConfig(nranks=8, timeout_s=120), body, devices=devices)
+        for name in ("bcast_replace", "reduce_sum"):
+            emit(ctx, {"config": 3, "op": name, "permuted": permute is not None, "N": N,
+                       "ranks": 8, "gpus": ng, "transport": "threads (peer copies)",
+                       "us_per_op_max_rank": max(g[name] for g in got)})
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--config", type=int, required=True)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--cpu", action="store_true")
+    p.add_argument("--max-bytes", type=int, default=256 << 20)
+    p.add_argument("--n3", type=int, default=400)
+    args = p.parse_args()
+    ctx = Ctx()
+    {1: config1, 3: config3, 4: config4, 5: config5}[args.config](ctx, args)
+    if ctx.dist:
+        ctx.dist.barrier()
+        ctx.dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -151,3 +151,19 @@ def random_graph(seed: int, nranks: int, max_vertices: int):
         pairs = out[p:p + 2 * nleaves].reshape(-1, 2); p += 2 * nleaves
         res.append((nroots, nleaves, local, pairs[:, 0].astype(np.int32).copy(), pairs[:, 1].copy()))
     return res
+
+
+def time_op(specs, opkind: str, dtype: str, op: str, steps: int, warmup: int = 1) -> dict:
+    """Mean microseconds per call of one operation on the reference CPU path."""
+    lib = _load()
+    if not getattr(lib, "_time_op_typed", False):
+        V, I = C.c_void_p, C.c_int
+        lib.sfref_time_op.argtypes = [I, V, V, V, V, V, I, I, I, I, I, V]
+        lib._time_op_typed = True
+    g = _Graph(specs)
+    out = np.zeros(2, np.float64)
+    kind = {"int32": 0, "int64": 1, "float64": 2}[dtype]
+    rc = lib.sfref_time_op(*g.args(), OPKIND[opkind], kind, OPS[op], steps, warmup, out.ctypes.data)
+    if rc != 0:
+        raise RuntimeError(lib.sfref_last_error().decode())
+    return {"setup_s": float(out[0]), "us_per_call": float(out[1])}

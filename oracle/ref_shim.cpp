@@ -180,6 +180,65 @@ int sfref_time_bcast_reduce(int nranks, const int64_t* nroots, const int64_t* nl
   }
 }
 
+// Time `steps` calls of one operation (opkind as sfref_run: 1 reduce, 2
+// fetch_and_op, 0 bcast) on the given kind with deterministic data. out[0] =
+// max SetUp s, out[1] = max over ranks of mean us per call.
+int sfref_time_op(int nranks, const int64_t* nroots, const int64_t* nleaves,
+                  const int64_t* const* local, const int32_t* const* rrank,
+                  const int64_t* const* roff, int opkind, int kind, int op, int steps, int warmup,
+                  double* out) {
+  try {
+    sf::RunConfig cfg;
+    cfg.nranks = nranks;
+    cfg.timeout_s = 3600.0;
+    std::vector<double> setup_s(static_cast<size_t>(nranks)), us(static_cast<size_t>(nranks));
+    sf::run_ranks(cfg, [&](sf::Comm& comm) {
+      using clk = std::chrono::steady_clock;
+      const int r = comm.rank();
+      sf::StarForest f(comm);
+      f.set_graph(make_spec(r, nroots, nleaves, local, rrank, roff));
+      const auto t0 = clk::now();
+      f.setup();
+      setup_s[static_cast<size_t>(r)] = std::chrono::duration<double>(clk::now() - t0).count();
+      const sf::Unit u{static_cast<sf::Kind>(kind), 1};
+      const size_t ub = u.bytes();
+      std::vector<unsigned char> root(static_cast<size_t>(nroots[r]) * ub + 8),
+          leaf(static_cast<size_t>(f.leaf_index_bound()) * ub + 8),
+          upd(static_cast<size_t>(f.leaf_index_bound()) * ub + 8);
+      for (size_t i = 0; i + ub <= root.size(); i += ub) {
+        if (kind == 2) { double v = 1.0; std::memcpy(&root[i], &v, 8); }
+        else root[i] = 1;
+      }
+      for (size_t i = 0; i + ub <= leaf.size(); i += ub) {
+        if (kind == 2) { double v = 0.5; std::memcpy(&leaf[i], &v, 8); }
+        else leaf[i] = 1;
+      }
+      const auto rop = static_cast<sf::ReduceOp>(op);
+      auto call = [&] {
+        switch (opkind) {
+          case 0: sf::bcast(f, u, root.data(), leaf.data(), rop); break;
+          case 1: sf::reduce(f, u, leaf.data(), root.data(), rop); break;
+          case 2: sf::fetch_and_op(f, u, root.data(), leaf.data(), upd.data(), rop); break;
+          default: throw sf::Error("unknown opkind");
+        }
+      };
+      for (int w = 0; w < warmup; ++w) call();
+      comm.barrier();
+      const auto s0 = clk::now();
+      for (int s = 0; s < steps; ++s) call();
+      const auto s1 = clk::now();
+      comm.barrier();
+      us[static_cast<size_t>(r)] = std::chrono::duration<double, std::micro>(s1 - s0).count() / steps;
+    });
+    out[0] = *std::max_element(setup_s.begin(), setup_s.end());
+    out[1] = *std::max_element(us.begin(), us.end());
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
 // The reference's splitmix64 stream and mix_seed (rng.hpp:14-51), to pin the
 // Python port used by the generators.
 int sfref_rng(uint64_t seed, int64_t n, uint64_t* out, uint64_t salt, uint64_t* mixed) {

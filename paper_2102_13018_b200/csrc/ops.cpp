@@ -103,10 +103,15 @@ struct Launch {
   LaunchParams p{};
   bool any_op = false;
 
-  void add(const DSeg& s, int64_t entries = 0) {
+  // entries: CSR contributions; src_distinct / dst_distinct: distinct
+  // indices of the two patterns (-1 = all distinct), for algorithmic bytes.
+  void add(const DSeg& s, int64_t entries = 0, int64_t src_distinct = -1,
+           int64_t dst_distinct = -1) {
     if (s.n <= 0) return;
     SFG_REQUIRE(p.nseg < kMaxSegs, "too many segments in one launch");
     csr_entries[p.nseg] = entries;
+    distinct_src[p.nseg] = src_distinct < 0 ? s.n : src_distinct;
+    distinct_dst[p.nseg] = dst_distinct < 0 ? s.n : dst_distinct;
     p.seg[p.nseg++] = s;
     if (!s.replace) any_op = true;
   }
@@ -172,10 +177,12 @@ struct Launch {
       const DSeg& g = p.seg[s];
       const double n = static_cast<double>(g.n);
       const double idx = 4.0 * n * ((g.src.kind == PAT_INDEXED) + (g.dst.kind == PAT_INDEXED));
+      const double ds = static_cast<double>(distinct_src[s]);
+      const double dd = static_cast<double>(distinct_dst[s]);
       switch (g.type) {
         case SEG_PAIR:
-        case SEG_PAIR_ATOMIC: b += n * ub * (g.replace ? 2.0 : 3.0) + idx; break;
-        case SEG_ATOMIC_FETCH: b += n * ub * 4.0 + idx; break;
+        case SEG_PAIR_ATOMIC: b += ds * ub + dd * ub * (g.replace ? 1.0 : 2.0) + idx; break;
+        case SEG_ATOMIC_FETCH: b += 2.0 * n * ub + 2.0 * dd * ub + idx; break;
         case SEG_CSR_FOLD:
         case SEG_CSR_FETCH: {
           const double e = static_cast<double>(csr_entries[s]);
@@ -189,6 +196,8 @@ struct Launch {
 
   const char* tag = "kernel";
   int64_t csr_entries[kMaxSegs] = {};
+  int64_t distinct_src[kMaxSegs] = {};
+  int64_t distinct_dst[kMaxSegs] = {};
 };
 
 void set_bufs(Launch& L, const OpHandle& h, void* root, void* leaf, const void* src_ro) {
@@ -280,7 +289,8 @@ void begin_phase(OpHandle& h, Launch& pack, Launch& local, const std::vector<Xfe
   c.fork(h.stream);
   const bool fuse = local.algorithmic_bytes(h.unit) < kFuseLocalBytes;
   if (fuse) {
-    for (int i = 0; i < local.p.nseg; ++i) pack.add(local.p.seg[i], local.csr_entries[i]);
+    for (int i = 0; i < local.p.nseg; ++i)
+      pack.add(local.p.seg[i], local.csr_entries[i], local.distinct_src[i], local.distinct_dst[i]);
     pack.tag = tag_of(h, 0);
   } else {
     pack.tag = tag_of(h, 2);
@@ -315,12 +325,14 @@ void begin_root_to_leaf(OpHandle& h) {
       sends.push_back({g.rank, const_cast<void*>(at(h.src, g.contig_start, ub)), static_cast<size_t>(g.n) * ub});
       counters().pack_elided++;
     } else {
-      pack.add(pair_seg(g.pat, BUF_ROOT, contig(g.stage_off), BUF_ROOT_STAGE, g.n, true));
+      pack.add(pair_seg(g.pat, BUF_ROOT, contig(g.stage_off), BUF_ROOT_STAGE, g.n, true), 0, g.distinct);
       sends.push_back({g.rank, at(h.stg->root_stage, g.stage_off, ub), static_cast<size_t>(g.n) * ub});
       counters().pack_copies++;
     }
   }
-  if (d.has_self) local.add(pair_seg(d.self_root, BUF_ROOT, d.self_leaf, BUF_LEAF, d.n_self, replace));
+  if (d.has_self)
+    local.add(pair_seg(d.self_root, BUF_ROOT, d.self_leaf, BUF_LEAF, d.n_self, replace), 0,
+              d.self_root_distinct);
 
   h.recvs.clear();
   h.zero_copy_recv.clear();
@@ -376,12 +388,14 @@ void begin_leaf_to_root(OpHandle& h) {
   if (d.has_self) {
     if (replace && d.self_root_dups) counters().replace_dup_collisions++;
     if (replace || !d.self_root_dups) {
-      local.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, replace));
+      local.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, replace), 0, -1,
+                d.self_root_distinct);
     } else if (det) {
       sf.ensure_csr();
       local.add(csr_seg(d, CsrRange::self_only, SEG_CSR_FOLD), d.csr_self_entries);
     } else {
-      local.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, false, true));
+      local.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, false, true), 0, -1,
+                d.self_root_distinct);
     }
   }
 
@@ -412,7 +426,8 @@ void end_leaf_to_root(OpHandle& h) {
       for (size_t k = 0; k < d.lg.size(); ++k) {
         if (h.zero_copy_recv[k]) continue;
         const auto& g = d.lg[k];
-        L.add(pair_seg(contig(g.stage_off), BUF_ROOT_STAGE, g.pat, BUF_ROOT, g.n, replace));
+        L.add(pair_seg(contig(g.stage_off), BUF_ROOT_STAGE, g.pat, BUF_ROOT, g.n, replace), 0, -1,
+              g.distinct);
         counters().unpack_copies++;
       }
     } else if (det) {
@@ -422,7 +437,8 @@ void end_leaf_to_root(OpHandle& h) {
       counters().unpack_copies += d.lg.size();
     } else {
       for (const auto& g : d.lg) {
-        L.add(pair_seg(contig(g.stage_off), BUF_ROOT_STAGE, g.pat, BUF_ROOT, g.n, false, true));
+        L.add(pair_seg(contig(g.stage_off), BUF_ROOT_STAGE, g.pat, BUF_ROOT, g.n, false, true), 0, -1,
+              g.distinct);
         counters().unpack_copies++;
       }
     }

@@ -179,21 +179,22 @@ std::vector<TimingRec> timing_collect() {
 
 namespace {
 
-bool has_dups(const std::vector<int64_t>& v, int64_t lo, int64_t hi) {
-  if (v.size() < 2) return false;
+int64_t count_distinct(const std::vector<int64_t>& v, int64_t lo, int64_t hi) {
+  if (v.size() < 2) return static_cast<int64_t>(v.size());
   const uint64_t span = static_cast<uint64_t>(hi - lo) + 1;
   if (span <= 4 * static_cast<uint64_t>(v.size()) + 4096) {
     std::vector<uint8_t> seen(span, 0);
+    int64_t d = 0;
     for (int64_t x : v) {
       uint8_t& s = seen[static_cast<size_t>(x - lo)];
-      if (s) return true;
+      d += s == 0;
       s = 1;
     }
-    return false;
+    return d;
   }
   std::vector<int64_t> sorted(v);
   std::sort(sorted.begin(), sorted.end());
-  return std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end();
+  return static_cast<int64_t>(std::unique(sorted.begin(), sorted.end()) - sorted.begin());
 }
 
 // Verify start + k*s2 + j*s1 + x over (dz, dy, dx).
@@ -217,6 +218,7 @@ Pattern Pattern::contiguous_range(int64_t start, int64_t n) {
   p.start = n == 0 ? 0 : start;
   p.count = n;
   p.bound = n == 0 ? 0 : start + n;
+  p.distinct = n;
   return p;
 }
 
@@ -239,6 +241,7 @@ Pattern Pattern::analyze(const int64_t* idx, int64_t n, bool infer_affine, int64
     p.s1 = s1;
     p.s2 = s2;
     p.bound = start + (dz - 1) * s2 + (dy - 1) * s1 + dx;
+    p.distinct = n;
     return p;
   };
 
@@ -286,7 +289,8 @@ Pattern Pattern::analyze(const int64_t* idx, int64_t n, bool infer_affine, int64
   }
   p.start = lo;
   p.bound = hi + 1;
-  p.has_duplicates = has_dups(p.idx, lo, hi);
+  p.distinct = count_distinct(p.idx, lo, hi);
+  p.has_duplicates = p.distinct < n;
   return p;
 }
 

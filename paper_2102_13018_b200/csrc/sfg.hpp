@@ -125,6 +125,7 @@ struct Pattern {
   int64_t dx = 0, dy = 0, dz = 0, s1 = 0, s2 = 0;  // affine
   std::vector<int64_t> idx;                         // indexed
   bool has_duplicates = false;
+  int64_t distinct = 0;  // number of distinct indices
   int64_t bound = 0;  // largest index + 1 (0 when empty)
 
   // extents_x / extents_xy > 0: reference-style detection with known extents.
@@ -289,7 +290,9 @@ struct DevPlan {
     DPat pat;
     bool contiguous;
     int64_t contig_start;
+    int64_t distinct;  // distinct indices of `pat`
   };
+  int64_t self_root_distinct = 0;
   std::vector<Seg> rg;  // remote root groups (I own the leaves)
   std::vector<Seg> lg;  // remote leaf groups (I own the roots)
   int64_t n_leafside = 0;  // total remote edges, leaf side

@@ -326,12 +326,13 @@ DevPlan& StarForest::dev() {
     d->self_root = dpat(leaf_groups_.front().pat);
     d->self_leaf = dpat(root_groups_.front().pat);
     d->self_root_dups = leaf_groups_.front().pat.has_duplicates;
+    d->self_root_distinct = leaf_groups_.front().pat.distinct;
   }
   int64_t off = 0;
   for (size_t gi = self ? 1 : 0; gi < root_groups_.size(); ++gi) {
     const auto& g = root_groups_[gi];
     const int64_t cnt = static_cast<int64_t>(g.items.size());
-    d->rg.push_back({g.rank, cnt, off, dpat(g.pat), g.pat.is_contiguous(), g.pat.start});
+    d->rg.push_back({g.rank, cnt, off, dpat(g.pat), g.pat.is_contiguous(), g.pat.start, g.pat.distinct});
     off += cnt;
   }
   d->n_leafside = off;
@@ -339,7 +340,7 @@ DevPlan& StarForest::dev() {
   for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size(); ++gi) {
     const auto& g = leaf_groups_[gi];
     const int64_t cnt = static_cast<int64_t>(g.items.size());
-    d->lg.push_back({g.rank, cnt, off, dpat(g.pat), g.pat.is_contiguous(), g.pat.start});
+    d->lg.push_back({g.rank, cnt, off, dpat(g.pat), g.pat.is_contiguous(), g.pat.start, g.pat.distinct});
     off += cnt;
   }
   d->n_rootside = off;
