@@ -332,6 +332,74 @@ __device__ __forceinline__ void run_csr(const DSeg& s, const LaunchParams& P, in
   }
 }
 
+// Warp-per-root CSR fold / fetch for high-degree roots. The 32 lanes load 32
+// consecutive contributions (coalesced entry reads); with csr_seq the fold
+// runs in exact entry order through shuffles (bit-identical to the sequential
+// reference for floating point), otherwise as a warp tree (fold) or inclusive
+// scan (fetch), exact for the associative integer ops.
+template <class T, int OP>
+__device__ __forceinline__ void run_csr_warp(const DSeg& s, const LaunchParams& P, int64_t blk,
+                                             bool fetch) {
+  T* root = static_cast<T*>(P.bufs[s.dst_buf]);
+  const T* leaf = static_cast<const T*>(P.bufs[s.src_buf]);
+  T* stage = static_cast<T*>(P.bufs[s.stage_buf]);
+  T* aux = static_cast<T*>(P.bufs[s.aux_buf]);
+  const int64_t bl = P.bl;
+  const int lane = threadIdx.x & 31;
+  const int64_t item = blk * (kThreads / 32) + (threadIdx.x >> 5);
+  if (item >= s.n * bl) return;
+  int64_t r, k;
+  const ItemMap im{bl, s.n * bl < (int64_t(1) << 31), P.bldiv};
+  im.split(item, r, k);
+  const int32_t lo = __ldg(s.csr_lo + r);
+  const int32_t hi = __ldg(s.csr_hi + r);
+  if (lo >= hi) return;
+  const int64_t ro = static_cast<int64_t>(__ldg(s.csr_roots + r)) * bl + k;
+  T acc = root[ro];
+  for (int32_t base = lo; base < hi; base += 32) {
+    const int32_t j = base + lane;
+    const int cnt = min(32, hi - base);
+    int32_t en = 0;
+    T v = T(0);
+    if (j < hi) {
+      en = __ldg(s.csr_ent + j);
+      v = en >= 0 ? leaf[static_cast<int64_t>(en) * bl + k]
+                  : stage[static_cast<int64_t>(-en - 1) * bl + k];
+    }
+    T mine = acc;
+    if (s.csr_seq) {
+      for (int q = 0; q < cnt; ++q) {
+        const T vq = __shfl_sync(0xffffffffu, v, q);
+        if (lane == q) mine = acc;
+        acc = apply_op<T, OP>(acc, vq);
+      }
+    } else if (!fetch) {
+      T x = v;
+      for (int off = 16; off > 0; off >>= 1) {
+        const T y = __shfl_down_sync(0xffffffffu, x, off);
+        if (lane + off < cnt) x = apply_op<T, OP>(x, y);
+      }
+      acc = apply_op<T, OP>(acc, __shfl_sync(0xffffffffu, x, 0));
+    } else {
+      T x = v;  // inclusive scan over lanes < cnt
+      for (int off = 1; off < 32; off <<= 1) {
+        const T y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off && lane < cnt) x = apply_op<T, OP>(y, x);
+      }
+      const T excl = __shfl_up_sync(0xffffffffu, x, 1);
+      mine = lane == 0 ? acc : apply_op<T, OP>(acc, excl);
+      acc = apply_op<T, OP>(acc, __shfl_sync(0xffffffffu, x, cnt - 1));
+    }
+    if (fetch && j < hi) {
+      if (en >= 0)
+        aux[static_cast<int64_t>(en) * bl + k] = mine;
+      else
+        stage[static_cast<int64_t>(-en - 1) * bl + k] = mine;
+    }
+  }
+  if (lane == 0) root[ro] = acc;
+}
+
 // Free-order fetch-and-op: fetched = atomic(root[dpat(i)] op= src[spat(i)]),
 // written to aux[spat(i)] (leafupdate for self edges, the reply slot in place
 // for remote contributions).
@@ -395,10 +463,20 @@ __global__ void __launch_bounds__(kThreads) segments_kernel(const __grid_constan
       }
       break;
     case SEG_CSR_FOLD:
-      if constexpr (OP != OP_REPLACE) run_csr<T, OP>(seg, P, blk, false);
+      if constexpr (OP != OP_REPLACE) {
+        if (seg.csr_warp)
+          run_csr_warp<T, OP>(seg, P, blk, false);
+        else
+          run_csr<T, OP>(seg, P, blk, false);
+      }
       break;
     case SEG_CSR_FETCH:
-      if constexpr (OP != OP_REPLACE) run_csr<T, OP>(seg, P, blk, true);
+      if constexpr (OP != OP_REPLACE) {
+        if (seg.csr_warp)
+          run_csr_warp<T, OP>(seg, P, blk, true);
+        else
+          run_csr<T, OP>(seg, P, blk, true);
+      }
       break;
     case SEG_ATOMIC_FETCH:
       if constexpr (OP != OP_REPLACE && sizeof(T) >= 4) run_atomic_fetch<T, OP>(seg, P, blk);
@@ -468,7 +546,8 @@ int launch_segments(LaunchParams& p, ElemType t, int op, cudaStream_t stream) {
     if (items <= 0) continue;
     p.seg[n] = p.seg[s];
     p.block_start[n] = blocks;
-    blocks += (items + kThreads * kItems - 1) / (kThreads * kItems);
+    const int64_t per_block = p.seg[s].csr_warp ? kThreads / 32 : kThreads * kItems;
+    blocks += (items + per_block - 1) / per_block;
     ++n;
   }
   p.nseg = n;

@@ -92,6 +92,12 @@ struct DSeg {
   const int32_t* csr_lo = nullptr;
   const int32_t* csr_hi = nullptr;
   const int32_t* csr_ent = nullptr;
+  // CSR execution: 0 = one thread per root item, 1 = one warp per root item
+  // (high degree). csr_seq = 1 forces the exact sequential fold order (float
+  // data in deterministic mode); otherwise integer/associative ops combine
+  // with a warp tree/scan, which is bit-identical for them.
+  int32_t csr_warp = 0;
+  int32_t csr_seq = 1;
 };
 
 constexpr int kMaxSegs = 12;

@@ -71,9 +71,16 @@ DSeg pair_seg(const DPat& src, int sbuf, const DPat& dst, int dbuf, int64_t n, b
 
 enum class CsrRange { self_only, remote_only, all };
 
-DSeg csr_seg(const DevPlan& d, CsrRange range, int32_t type) {
+// seq: keep the exact sequential fold order inside a warp (float data in
+// deterministic mode). High-degree roots get a warp each.
+DSeg csr_seg(const DevPlan& d, CsrRange range, int32_t type, bool seq) {
   DSeg s;
   s.type = type;
+  const int64_t entries = range == CsrRange::self_only ? d.csr_self_entries
+                          : range == CsrRange::remote_only ? d.csr_remote_entries
+                                                           : d.csr_self_entries + d.csr_remote_entries;
+  s.csr_warp = d.csr_n > 0 && entries >= 8 * d.csr_n ? 1 : 0;
+  s.csr_seq = seq ? 1 : 0;
   s.n = d.csr_n;
   s.src_buf = BUF_SRC_RO;
   s.dst_buf = BUF_ROOT;
@@ -256,6 +263,23 @@ void end_common(OpHandle& h) {
   h.stg = nullptr;
 }
 
+// Root-sorted CSR execution is always used in deterministic mode; in
+// free-order mode it replaces atomics when roots have high degree (>= 8
+// contributions on average), where a warp per root beats contended atomics.
+bool prefer_csr(StarForest& sf, bool det, CsrRange range) {
+  sf.ensure_csr();
+  if (det) return true;
+  const DevPlan& d = sf.dev();
+  const int64_t e = range == CsrRange::self_only ? d.csr_self_entries
+                    : range == CsrRange::remote_only ? d.csr_remote_entries
+                                                     : d.csr_self_entries + d.csr_remote_entries;
+  return d.csr_n > 0 && e >= 8 * d.csr_n;
+}
+
+// Exact sequential order is only needed for floating point; integer ops are
+// associative under wrap-around, so tree/scan orders give identical bits.
+bool exact_seq(const OpHandle& h, bool det) { return det && h.unit.kind == Kind::float64; }
+
 // ------------------------------------------------------------ exchange phases
 //
 // Begin: the comm stream forks from the caller's stream, packs every remote
@@ -390,9 +414,8 @@ void begin_leaf_to_root(OpHandle& h) {
     if (replace || !d.self_root_dups) {
       local.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, replace), 0, -1,
                 d.self_root_distinct);
-    } else if (det) {
-      sf.ensure_csr();
-      local.add(csr_seg(d, CsrRange::self_only, SEG_CSR_FOLD), d.csr_self_entries);
+    } else if (prefer_csr(sf, det, CsrRange::self_only)) {
+      local.add(csr_seg(d, CsrRange::self_only, SEG_CSR_FOLD, exact_seq(h, det)), d.csr_self_entries);
     } else {
       local.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, false, true), 0, -1,
                 d.self_root_distinct);
@@ -430,10 +453,10 @@ void end_leaf_to_root(OpHandle& h) {
               g.distinct);
         counters().unpack_copies++;
       }
-    } else if (det) {
+    } else if (prefer_csr(sf, det, CsrRange::remote_only)) {
       // Ascending-rank fold of every remote contribution (ops.cpp:372-376).
-      sf.ensure_csr();
-      L.add(csr_seg(d, CsrRange::remote_only, SEG_CSR_FOLD), d.csr_remote_entries);
+      L.add(csr_seg(d, CsrRange::remote_only, SEG_CSR_FOLD, exact_seq(h, det)),
+            d.csr_remote_entries);
       counters().unpack_copies += d.lg.size();
     } else {
       for (const auto& g : d.lg) {
@@ -485,9 +508,9 @@ void end_fetch(OpHandle& h) {
     Launch L;
     L.tag = "fetch_end";
     set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
-    if (det) {
-      sf.ensure_csr();
-      L.add(csr_seg(d, CsrRange::all, SEG_CSR_FETCH), d.csr_self_entries + d.csr_remote_entries);
+    if (prefer_csr(sf, det, CsrRange::all)) {
+      L.add(csr_seg(d, CsrRange::all, SEG_CSR_FETCH, exact_seq(h, det)),
+            d.csr_self_entries + d.csr_remote_entries);
     } else {
       if (d.has_self) {
         DSeg s = pair_seg(d.self_leaf, BUF_SRC_RO, d.self_root, BUF_ROOT, d.n_self, false);
