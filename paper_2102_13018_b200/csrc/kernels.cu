@@ -356,16 +356,31 @@ __device__ __forceinline__ void run_csr_warp(const DSeg& s, const LaunchParams& 
   if (lo >= hi) return;
   const int64_t ro = static_cast<int64_t>(__ldg(s.csr_roots + r)) * bl + k;
   T acc = root[ro];
-  for (int32_t base = lo; base < hi; base += 32) {
+  constexpr int kChunks = 8;  // 256 contributions in flight per warp
+  for (int32_t sbase = lo; sbase < hi; sbase += 32 * kChunks) {
+    int32_t ens[kChunks];
+    T vs[kChunks];
+#pragma unroll
+    for (int c = 0; c < kChunks; ++c) {
+      const int32_t j = sbase + 32 * c + lane;
+      ens[c] = j < hi ? __ldg(s.csr_ent + j) : 0;
+    }
+#pragma unroll
+    for (int c = 0; c < kChunks; ++c) {
+      const int32_t j = sbase + 32 * c + lane;
+      vs[c] = T(0);
+      if (j < hi)
+        vs[c] = ens[c] >= 0 ? leaf[static_cast<int64_t>(ens[c]) * bl + k]
+                            : stage[static_cast<int64_t>(-ens[c] - 1) * bl + k];
+    }
+#pragma unroll
+    for (int c = 0; c < kChunks; ++c) {
+    const int32_t base = sbase + 32 * c;
+    if (base >= hi) break;
     const int32_t j = base + lane;
     const int cnt = min(32, hi - base);
-    int32_t en = 0;
-    T v = T(0);
-    if (j < hi) {
-      en = __ldg(s.csr_ent + j);
-      v = en >= 0 ? leaf[static_cast<int64_t>(en) * bl + k]
-                  : stage[static_cast<int64_t>(-en - 1) * bl + k];
-    }
+    const int32_t en = ens[c];
+    const T v = vs[c];
     T mine = acc;
     if (s.csr_seq) {
       for (int q = 0; q < cnt; ++q) {
@@ -395,6 +410,7 @@ __device__ __forceinline__ void run_csr_warp(const DSeg& s, const LaunchParams& 
         aux[static_cast<int64_t>(en) * bl + k] = mine;
       else
         stage[static_cast<int64_t>(-en - 1) * bl + k] = mine;
+    }
     }
   }
   if (lane == 0) root[ro] = acc;

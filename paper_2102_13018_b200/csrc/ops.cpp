@@ -20,6 +20,7 @@
 // ascending leaf index (ops.cpp:364,372-376; oracle.cpp:84-90) — so
 // floating-point results are bit-identical to the CPU reference. The
 // free-order mode uses atomics (pack.cpp:47-58 "atomics" mode).
+#include <cstdlib>
 #include <cstring>
 
 #include "sfg.hpp"
@@ -267,6 +268,10 @@ void end_common(OpHandle& h) {
 // free-order mode it replaces atomics when roots have high degree (>= 8
 // contributions on average), where a warp per root beats contended atomics.
 bool prefer_csr(StarForest& sf, bool det, CsrRange range) {
+  if (!det) {
+    static const bool atomics_only = std::getenv("SFG_FREE_ORDER_ATOMICS") != nullptr;
+    if (atomics_only) return false;
+  }
   sf.ensure_csr();
   if (det) return true;
   const DevPlan& d = sf.dev();
