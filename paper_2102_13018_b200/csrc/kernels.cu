@@ -449,7 +449,10 @@ __device__ __forceinline__ void run_atomic_fetch(const DSeg& s, const LaunchPara
   }
 }
 
-template <class T, int OP>
+// FULL = the launch contains root-sorted (CSR) or fetch segments. Pair-only
+// launches (every pack, unpack and structured local scatter) get their own
+// instantiation so the CSR paths do not raise their register allocation.
+template <class T, int OP, bool FULL>
 __global__ void __launch_bounds__(kThreads) segments_kernel(const __grid_constant__ LaunchParams P) {
   const int64_t b = blockIdx.x;
   int s = 0;
@@ -479,7 +482,7 @@ __global__ void __launch_bounds__(kThreads) segments_kernel(const __grid_constan
       }
       break;
     case SEG_CSR_FOLD:
-      if constexpr (OP != OP_REPLACE) {
+      if constexpr (OP != OP_REPLACE && FULL) {
         if (seg.csr_warp)
           run_csr_warp<T, OP>(seg, P, blk, false);
         else
@@ -487,7 +490,7 @@ __global__ void __launch_bounds__(kThreads) segments_kernel(const __grid_constan
       }
       break;
     case SEG_CSR_FETCH:
-      if constexpr (OP != OP_REPLACE) {
+      if constexpr (OP != OP_REPLACE && FULL) {
         if (seg.csr_warp)
           run_csr_warp<T, OP>(seg, P, blk, true);
         else
@@ -495,7 +498,7 @@ __global__ void __launch_bounds__(kThreads) segments_kernel(const __grid_constan
       }
       break;
     case SEG_ATOMIC_FETCH:
-      if constexpr (OP != OP_REPLACE && sizeof(T) >= 4) run_atomic_fetch<T, OP>(seg, P, blk);
+      if constexpr (OP != OP_REPLACE && sizeof(T) >= 4 && FULL) run_atomic_fetch<T, OP>(seg, P, blk);
       break;
     default:
       break;
@@ -504,7 +507,17 @@ __global__ void __launch_bounds__(kThreads) segments_kernel(const __grid_constan
 
 template <class T, int OP>
 void launch_t(const LaunchParams& p, int64_t blocks, cudaStream_t st) {
-  segments_kernel<T, OP><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
+  bool full = false;
+  for (int s = 0; s < p.nseg; ++s)
+    full = full || (p.seg[s].type != SEG_PAIR && p.seg[s].type != SEG_PAIR_ATOMIC);
+  if constexpr (OP == OP_REPLACE) {
+    segments_kernel<T, OP, false><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
+  } else {
+    if (full)
+      segments_kernel<T, OP, true><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
+    else
+      segments_kernel<T, OP, false><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
+  }
 }
 
 template <class T>
