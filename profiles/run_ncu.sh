@@ -1,13 +1,15 @@
 #!/bin/bash
 # ncu evidence for the bench's kernels (run under gpurun on ONE GPU).
 # 1) launch list (per-launch device time, cold cache, serialised)
-# 2) one --set full capture of the two hot launches (bcast_begin, reduce_begin)
+# 2) one --set full capture of the two hot launches (bcast, reduce)
+# usage: bash profiles/run_ncu.sh <outdir> <tag>
 set -e
 OUT=${1:-gpurun_out}
+TAG=${2:-r1}
 CMD="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e"
-$CMD > $OUT/plain.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1
+$CMD > $OUT/plain_$TAG.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launches_$TAG.log 2>&1
 CMD2="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
-$CMD2 > $OUT/plain2.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:segments_kernel -s 6 -c 2 -o $OUT/prof_r1 $CMD2 > $OUT/ncu_full.log 2>&1
+$CMD2 > $OUT/plain2_$TAG.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:segments_kernel -s 6 -c 2 -o $OUT/prof_$TAG $CMD2 > $OUT/ncu_full_$TAG.log 2>&1
 echo done
