@@ -95,8 +95,12 @@ DSeg csr_seg(const DevPlan& d, CsrRange range, int32_t type, bool seq) {
       s.csr_hi = d.csr_split;
       break;
     case CsrRange::remote_only:
-      s.csr_lo = d.csr_split;
-      s.csr_hi = d.csr_off + 1;
+      s.n = d.rcsr_n;
+      s.csr_roots = d.rcsr_roots;
+      s.csr_ent = d.rcsr_ent;
+      s.csr_lo = d.rcsr_off;
+      s.csr_hi = d.rcsr_off + 1;
+      s.csr_warp = d.rcsr_n > 0 && entries >= 8 * d.rcsr_n ? 1 : 0;
       break;
     case CsrRange::all:
       s.csr_lo = d.csr_off;

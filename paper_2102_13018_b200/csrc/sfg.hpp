@@ -309,6 +309,11 @@ struct DevPlan {
   int32_t* csr_ent = nullptr;
   int64_t csr_self_entries = 0;
   int64_t csr_remote_entries = 0;
+  // remote-only CSR: just the roots that receive remote contributions
+  int64_t rcsr_n = 0;
+  int32_t* rcsr_roots = nullptr;
+  int32_t* rcsr_off = nullptr;  // [rcsr_n + 1]
+  int32_t* rcsr_ent = nullptr;
   ~DevPlan();
 };
 

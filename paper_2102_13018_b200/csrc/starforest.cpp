@@ -416,7 +416,22 @@ void StarForest::ensure_csr() {
   d.csr_n = static_cast<int64_t>(roots.size());
   d.csr_self_entries = self ? static_cast<int64_t>(leaf_groups_.front().items.size()) : 0;
   d.csr_remote_entries = total - d.csr_self_entries;
-  const size_t bytes = (roots.size() + offs.size() + split.size() + ent.size()) * sizeof(int32_t);
+
+  // Remote-only view: the (usually few) roots with remote contributions, so
+  // the End-side fold does not walk every root of the forest.
+  std::vector<int32_t> rroots, roffs, rent;
+  for (size_t q = 0; q < roots.size(); ++q) {
+    const int32_t a = split[q], b = offs[q + 1];
+    if (a == b) continue;
+    rroots.push_back(roots[q]);
+    roffs.push_back(static_cast<int32_t>(rent.size()));
+    rent.insert(rent.end(), ent.begin() + a, ent.begin() + b);
+  }
+  roffs.push_back(static_cast<int32_t>(rent.size()));
+  d.rcsr_n = static_cast<int64_t>(rroots.size());
+
+  const size_t bytes = (roots.size() + offs.size() + split.size() + ent.size() + rroots.size() +
+                        roffs.size() + rent.size()) * sizeof(int32_t);
   if (bytes) {
     SFG_CUDA(cudaMalloc(&d.csr_blob, bytes));
     auto* p = static_cast<int32_t*>(d.csr_blob);
@@ -429,6 +444,9 @@ void StarForest::ensure_csr() {
     put(offs, d.csr_off);
     put(split, d.csr_split);
     put(ent, d.csr_ent);
+    put(rroots, d.rcsr_roots);
+    put(roffs, d.rcsr_off);
+    put(rent, d.rcsr_ent);
   }
   d.csr_built = true;
 }
