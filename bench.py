@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--sample-steps", type=int, default=10)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                   help="remote exchange at N>1: one-sided NVLink puts (p2p) or grouped NCCL send/recv")
     return p.parse_args()
 
 
@@ -200,7 +202,8 @@ def ours(args, rank, world, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         obj = [sf.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        comm = sf.Comm(world, rank, dev, sf.CommConfig(nranks=world, backend="nccl"), nccl_id=obj[0])
+        comm = sf.Comm(world, rank, dev, sf.CommConfig(nranks=world, backend=args.transport),
+                       nccl_id=obj[0])
     else:
         dist = None
         comm = sf.Comm(1, 0, dev, sf.CommConfig(nranks=1, backend="threads"))
@@ -277,7 +280,8 @@ def ours(args, rank, world, local):
 
     # roofline of the dominant kernel (largest device time in the region)
     peak, peak_kind = peaks()
-    dom_tag, dom = max(timing.items(), key=lambda kv: kv[1]["total_ms"])
+    dom_tag, dom = max(((k, v) for k, v in timing.items() if v["bytes"] > 0),
+                       key=lambda kv: kv[1]["total_ms"])
     per_launch_bytes = dom["bytes"] / dom["launches"]
     per_launch_ms = dom["total_ms"] / dom["launches"]
     achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
@@ -289,6 +293,22 @@ def ours(args, rank, world, local):
         except Exception:
             traffic = None
     share = dom["total_ms"] / max(1e-9, ev0.elapsed_time(ev1))
+
+    # remote exchange over NVLink: bytes this rank stored into / sent to its
+    # peers per exchange interval (p2p: the put kernels; nccl: the grouped
+    # send/recv on the comm stream), slowest rank reported
+    link_recs = [v for v in timing.values() if v.get("link_bytes", 0) > 0]
+    nvlink = None
+    if world > 1:
+        lb = sum(v["link_bytes"] for v in link_recs)
+        lms = sum(v["total_ms"] for v in link_recs)
+        gbs = lb / (lms * 1e-3) / 1e9 if lms > 0 else 0.0
+        gmin = -allreduce(-gbs, "max")
+        lus = allreduce(1e3 * lms / max(1, sum(v["launches"] for v in link_recs)), "max")
+        nvlink = {"achieved": gmin, "peak": 900.0, "peak_kind": "nominal per direction per GPU",
+                  "measured_peer_copy": 770.0, "unit": "GB/s", "frac": gmin / 900.0,
+                  "bytes_per_exchange": lb / max(1, sum(v["launches"] for v in link_recs)),
+                  "us_per_exchange": lus}
 
     # end-to-end: root vector from pinned host memory in, result back out
     e2e = None
@@ -337,7 +357,7 @@ def ours(args, rank, world, local):
                        "bytes_per_step": bytes_all, "nvlink_bytes_per_step": net_bytes,
                        "l2": "inputs > L2: 1.07 GB roots + 1.09 GB leaves per rank at N=1",
                        "setup_s": setup_s, "graph_gen_s": gen_s, "deterministic": True,
-                       "transport": "nccl" if world > 1 else "none (self edges only)"},
+                       "transport": args.transport if world > 1 else "none (self edges only)"},
             "gpu_launches": int(kl),
             "roofline": {"bound": "hbm", "kernel": dom_tag, "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
@@ -346,6 +366,7 @@ def ours(args, rank, world, local):
             "kernels": {k: {"launches": v["launches"], "us_per_launch": 1e3 * v["total_ms"] / v["launches"],
                             "GBps": v["bytes"] / (v["total_ms"] * 1e-3) / 1e9 if v["total_ms"] else None}
                         for k, v in timing.items()},
+            "nvlink": nvlink,
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -34,7 +34,8 @@ def env():
 
 
 class Ctx:
-    def __init__(self, deterministic=True):
+    def __init__(self, deterministic=True, transport="p2p"):
+        self.transport = transport
         import torch
 
         from paper_2102_13018_b200 import sf
@@ -61,7 +62,8 @@ class Ctx:
             obj = [sf.nccl_unique_id() if self.rank == 0 else None]
             self.dist.broadcast_object_list(obj, src=0)
             c = sf.Comm(self.world, self.rank, self.local,
-                        sf.CommConfig(nranks=self.world, backend="nccl", deterministic=deterministic),
+                        sf.CommConfig(nranks=self.world, backend=self.transport,
+                                      deterministic=deterministic),
                         nccl_id=obj[0])
         else:
             c = sf.Comm(1, 0, self.local, sf.CommConfig(nranks=1, deterministic=deterministic))
@@ -86,7 +88,7 @@ class Ctx:
         self.dist.all_reduce(t)
         return float(t.item())
 
-    def timed(self, fn, steps, warmup):
+    def timed(self, fn, steps, warmup, flush=True):
         torch, sf = self.torch, self.sf
         with torch.cuda.stream(self.stream):
             for _ in range(warmup):
@@ -96,13 +98,14 @@ class Ctx:
         sf.timing_collect()
         # Flush L2 (write 256 MB) before every timed call: the config-1/4
         # working sets fit in the 126 MB L2 and would otherwise be timed hot.
-        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(steps)]
         sf.timing_enable(True)
         with torch.cuda.stream(self.stream):
             for e0, e1 in evs:
-                flush.zero_()
+                if flush:
+                    flush_buf.zero_()
                 e0.record(self.stream)
                 fn()
                 e1.record(self.stream)
@@ -113,6 +116,42 @@ class Ctx:
         byts = self.vsum(sum(v["bytes"] for v in rec.values()) / steps)
         self.barrier()
         return ms, byts, rec
+
+
+def timed_graph(ctx, fn, steps, warmup, reps=5):
+    """Device-side time per call: `steps` calls captured into one CUDA graph
+    (the library's work is all stream-ordered kernels / NCCL calls, no host
+    synchronisation), replayed `reps` times; median per call, max over ranks.
+    Removes the Python/ctypes launch overhead that bounds latency-size
+    operations when they are issued eagerly."""
+    torch = ctx.torch
+    with torch.cuda.stream(ctx.stream):
+        for _ in range(warmup):
+            fn()
+    torch.cuda.synchronize()
+    ctx.barrier()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=ctx.stream):
+        for _ in range(steps):
+            fn()
+    torch.cuda.synchronize()
+    ctx.barrier()
+    g.replay()
+    torch.cuda.synchronize()
+    ctx.barrier()
+    per = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ctx.barrier()
+        with torch.cuda.stream(ctx.stream):
+            e0.record(ctx.stream)
+            g.replay()
+            e1.record(ctx.stream)
+        torch.cuda.synchronize()
+        per.append(e0.elapsed_time(e1) / steps)
+    ctx.barrier()
+    del g
+    return ctx.vmax(statistics.median(per))
 
 
 def peak():
@@ -133,9 +172,19 @@ def op_line(ctx, config, name, ms, byts, rec, extra=None):
     d = {"config": config, "op": name, "n_gpus": ctx.world, "us_per_op": ms * 1e3,
          "GBps": gbs, "frac_hbm": gbs / peak() if ctx.world == 1 else None,
          "kernels": {k: {"launches": v["launches"], "us": 1e3 * v["total_ms"] / v["launches"],
-                         "GBps": v["bytes"] / max(1e-12, v["total_ms"] * 1e-3) / 1e9}
+                         "GBps": v["bytes"] / max(1e-12, v["total_ms"] * 1e-3) / 1e9,
+                         "link_GBps": v.get("link_bytes", 0) / max(1e-12, v["total_ms"] * 1e-3) / 1e9}
                      for k, v in rec.items()},
          "dominant": dom[0]}
+    lrec = [v for v in rec.values() if v.get("link_bytes", 0) > 0]
+    if ctx.world > 1:
+        lb = sum(v["link_bytes"] for v in lrec)
+        lms = sum(v["total_ms"] for v in lrec)
+        g = lb / (lms * 1e-3) / 1e9 if lms > 0 else 0.0
+        d["transport"] = ctx.transport
+        d["nvlink"] = {"GBps_min_rank": -ctx.vmax(-g), "frac_of_900": -ctx.vmax(-g) / 900.0,
+                       "bytes_per_op_rank0": lb / max(1, sum(v["launches"] for v in lrec)),
+                       "us_exchange_max_rank": ctx.vmax(1e3 * lms / max(1, sum(v["launches"] for v in lrec)))}
     d.update(extra or {})
     emit(ctx, d)
 
@@ -182,6 +231,40 @@ def config1(ctx, args):
                 t = ref.time_op(specs, opk, "float64", op, 3, 1)
                 emit(ctx, {"config": 1, "op": f"{opk}_{op}", "impl": "reference_cpu", "cores": 1,
                            "us_per_op": t["us_per_call"], "setup_s": t["setup_s"]})
+
+
+# ------------------------------------------------------------------ config 2
+def config2(ctx, args):
+    """Halo-only variant (ii) of config 2: the ghost-face
+    SF of the 512^3 grid without the interior self edges, so Bcast/Reduce are
+    pure remote exchanges (pack -> NVLink -> unpack). Latency-reported."""
+    from paper_2102_13018_b200 import graphs
+
+    torch, sf = ctx.torch, ctx.sf
+    N = args.n2
+    spec = graphs.g2l_halo(N, ctx.world, ctx.rank, interior=False)
+    geo = graphs.G2L(N, ctx.world, ctx.rank)
+    f, setup_s = setup_forest(ctx, spec)
+    u = sf.Unit(sf.Kind.float64)
+    root = torch.rand(geo.n_owned, dtype=torch.float64, device="cuda")
+    leaf = torch.zeros(geo.n_local, dtype=torch.float64, device="cuda")
+
+    def bc():
+        h = sf.bcast_begin(f, u, root, leaf, sf.ReduceOp.replace, ctx.stream)
+        sf.bcast_end(h)
+
+    def rd():
+        h = sf.reduce_begin(f, u, leaf, root, sf.ReduceOp.sum, ctx.stream)
+        sf.reduce_end(h)
+
+    for name, fn in (("bcast_replace", bc), ("reduce_sum", rd)):
+        ms, byts, rec = ctx.timed(fn, args.steps, args.warmup, flush=False)
+        gms = timed_graph(ctx, fn, args.steps, args.warmup)
+        nbytes = ctx.vmax(float(sum(v.get("link_bytes", 0) for v in rec.values()) / args.steps))
+        op_line(ctx, 2, name, ms, byts, rec, {"variant": "halo-only", "grid": [N] * 3,
+                                               "nleaves_rank0": int(spec.nleaves), "setup_s": setup_s,
+                                               "graph_us_per_op": gms * 1e3,
+                                               "graph_link_GBps_max_rank_egress": nbytes / (gms * 1e-3) / 1e9})
 
 
 # ------------------------------------------------------------------ config 4
@@ -261,15 +344,27 @@ def config5(ctx, args):
         ok = True
         if ctx.rank == 1:
             ok = bool((leaf.cpu() == torch.arange(n)).all()) if n else True
+
+        def rt():
+            h = sf.bcast_begin(f, u, root, leaf, sf.ReduceOp.replace, ctx.stream)
+            sf.bcast_end(h)
+            h = sf.reduce_begin(f, u, leaf, root, sf.ReduceOp.replace, ctx.stream)
+            sf.reduce_end(h)
+
+        graph_half = timed_graph(ctx, rt, 20 if size <= (1 << 22) else 4, 2) * 1e3 / 2
+        if ctx.rank == 1:
+            ok = ok and (bool((leaf.cpu() == torch.arange(n)).all()) if n else True)
         dmed = ctx.vmax(statistics.median(dev_us))
         dmin = ctx.vmax(min(dev_us))
         hmed = ctx.vmax(statistics.median(host_us))
         rows.append({"bytes": size, "half_rtt_us_median": dmed, "half_rtt_us_min": dmin,
                      "host_half_rtt_us_median": hmed, "GBps": size / (dmed * 1e-6) / 1e9,
+                     "graph_half_rtt_us": graph_half, "graph_GBps": size / (graph_half * 1e-6) / 1e9,
                      "payload_ok": ok})
         del f
         size *= 2
-    emit(ctx, {"config": 5, "op": "pingpong_bcast+reduce_replace", "n_gpus": 2, "rows": rows})
+    emit(ctx, {"config": 5, "op": "pingpong_bcast+reduce_replace", "n_gpus": 2,
+               "transport": ctx.transport, "rows": rows})
 
 
 # ------------------------------------------------------------------ config 3
@@ -353,9 +448,11 @@ def main():
     p.add_argument("--cpu", action="store_true")
     p.add_argument("--max-bytes", type=int, default=256 << 20)
     p.add_argument("--n3", type=int, default=400)
+    p.add_argument("--n2", type=int, default=512)
+    p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"])
     args = p.parse_args()
-    ctx = Ctx()
-    {1: config1, 3: config3, 4: config4, 5: config5}[args.config](ctx, args)
+    ctx = Ctx(transport=args.transport)
+    {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}[args.config](ctx, args)
     if ctx.dist:
         ctx.dist.barrier()
         ctx.dist.destroy_process_group()

@@ -99,7 +99,11 @@ int sfg_nccl_unique_id(void* out, size_t bytes);
  * comm.cpp:138-143). world != NULL: ranks are threads of this process and the
  * control plane is in-process; world == NULL and nranks > 1: one process per
  * GPU, control plane over NCCL (nccl_id required). backend: "threads"
- * (stream-ordered peer copies, needs a world when nranks > 1) or "nccl".
+ * (stream-ordered peer copies, needs a world when nranks > 1), "nccl"
+ * (grouped ncclSend/ncclRecv) or "p2p" (one-sided puts into the peer GPU's
+ * staging mapped over NVLink with in-kernel flag signalling — the
+ * reference's onesided engine, ops.cpp:91,160-246; one GPU per rank; NCCL
+ * then only carries the control plane of process-per-GPU runs).
  * device < 0 creates a host-only communicator (set_graph/setup/degrees work,
  * operations do not). */
 int sfg_comm_create(sfg_world world, int nranks, int rank, int device, const char* backend,
@@ -176,12 +180,14 @@ int sfg_counters_reset(void);
 /* Per-launch device timing: when enabled, CUDA events are recorded on the
  * launching stream around every kernel of the library; collect() waits for
  * them and aggregates per launch tag ("bcast_begin", "reduce_end", ...),
- * with the launch's algorithmic bytes (compulsory HBM traffic). */
+ * with the launch's algorithmic bytes (compulsory HBM traffic) and the bytes
+ * it stored over NVLink into peer GPUs (one-sided puts of the p2p backend). */
 typedef struct sfg_timing {
   char tag[32];
   uint64_t launches;
   double total_ms;
   double bytes;
+  double link_bytes; /* bytes stored into peer GPUs' memory (p2p puts) */
 } sfg_timing;
 int sfg_timing_enable(int on);
 int sfg_timing_collect(sfg_timing* out, int cap, int* n);

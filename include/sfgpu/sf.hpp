@@ -89,7 +89,7 @@ struct TwoSidedInfo {
 
 struct CommConfig {
   int nranks = 1;
-  std::string backend = "threads";  // threads | nccl
+  std::string backend = "threads";  // threads | nccl | p2p
   bool deterministic = true;
   bool debug_checksum = false;
   bool force_remote = false;

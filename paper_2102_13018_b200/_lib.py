@@ -124,7 +124,7 @@ _SIGS = {
 
 class sfg_timing(C.Structure):
     _fields_ = [("tag", C.c_char * 32), ("launches", C.c_uint64), ("total_ms", C.c_double),
-                ("bytes", C.c_double)]
+                ("bytes", C.c_double), ("link_bytes", C.c_double)]
 
 EXPORTED = tuple(_SIGS)
 

@@ -173,8 +173,8 @@ sfg::CommConfig to_config(const sfg_config* cfg, const char* backend) {
     cc.timeout_s = cfg->timeout_s;
   }
   cc.backend = backend ? backend : "threads";
-  SFG_REQUIRE(cc.backend == "threads" || cc.backend == "nccl",
-              "unknown transport backend '" + cc.backend + "' (threads | nccl)");
+  SFG_REQUIRE(cc.backend == "threads" || cc.backend == "nccl" || cc.backend == "p2p",
+              "unknown transport backend '" + cc.backend + "' (threads | nccl | p2p)");
   return cc;
 }
 
@@ -195,7 +195,10 @@ sfg_comm make_comm(sfg_world world, int nranks, int rank, int device, const sfg:
     SFG_CUDA(cudaSetDevice(device));
     SFG_CUDA(cudaFree(nullptr));  // create the context
   }
-  if (cc.backend == "nccl") {
+  if (cc.backend == "p2p") SFG_REQUIRE(device >= 0, "the p2p backend needs a device");
+  // p2p: NCCL only carries the control plane (SetUp, slot mapping) when the
+  // ranks are processes without caller-supplied callbacks.
+  if (cc.backend == "nccl" || (cc.backend == "p2p" && !w && !ops && nranks > 1)) {
     SFG_REQUIRE(device >= 0, "the nccl backend needs a device");
     ncclUniqueId id;
     if (nccl_id) {
@@ -216,7 +219,7 @@ sfg_comm make_comm(sfg_world world, int nranks, int rank, int device, const sfg:
     SFG_REQUIRE(c.nccl_ != nullptr, "nranks > 1 without a world needs the nccl backend or control-plane callbacks");
     c.ctrl_ = sfg::make_nccl_ctrl(c.nccl_, rank, nranks, device);
   }
-  if (device >= 0) {
+  if (device >= 0 && cc.backend != "p2p") {
     if (cc.backend == "nccl")
       c.transport_ = sfg::make_nccl_transport(c.nccl_, rank, device);
     else
@@ -447,6 +450,7 @@ int sfg_timing_collect(sfg_timing* out, int cap, int* n) {
       out[k].launches = r.launches;
       out[k].total_ms = r.total_ms;
       out[k].bytes = r.bytes;
+      out[k].link_bytes = r.link_bytes;
       ++k;
     }
     *n = k;

@@ -14,6 +14,7 @@
 //   unpack:   /root/reference/proj/src/pack.cpp:138-173
 //   scatter:  /root/reference/proj/src/pack.cpp:220-256
 //   fetch:    /root/reference/proj/src/ops.cpp:110-158, 521-563
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <type_traits>
@@ -272,6 +273,51 @@ __device__ __forceinline__ void run_pair_rows(const DSeg& s, const LaunchParams&
 // Root-sorted fold in the reference order (self leaves ascending, then remote
 // groups ascending rank, each in ascending leaf order). Sequential per root,
 // so floating-point results are bit-identical to the CPU reference.
+// Sequential fold of contributions [lo, hi) of one root item by one thread,
+// 8 contributions in flight (entries, then values, then the dependent fold).
+template <class T, int OP>
+__device__ __forceinline__ T csr_thread_range(const DSeg& s, const T* leaf, T* stage, T* aux,
+                                              int64_t bl, int64_t k, int32_t lo, int32_t hi, T acc,
+                                              bool fetch) {
+  constexpr int kB = 8;
+  for (int32_t j = lo; j < hi; j += kB) {
+    int32_t en[kB];
+    T c[kB];
+#pragma unroll
+    for (int q = 0; q < kB; ++q) en[q] = j + q < hi ? __ldg(s.csr_ent + j + q) : 0;
+#pragma unroll
+    for (int q = 0; q < kB; ++q)
+      if (j + q < hi)
+        c[q] = en[q] >= 0 ? leaf[static_cast<int64_t>(en[q]) * bl + k]
+                          : stage[static_cast<int64_t>(-en[q] - 1) * bl + k];
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      if (j + q >= hi) break;
+      if (fetch) {
+        if (en[q] >= 0)
+          aux[static_cast<int64_t>(en[q]) * bl + k] = acc;
+        else
+          stage[static_cast<int64_t>(-en[q] - 1) * bl + k] = acc;
+      }
+      acc = apply_op<T, OP>(acc, c[q]);
+    }
+  }
+  return acc;
+}
+
+// Bounds of piece q of root r (see DSeg::csr_np).
+__device__ __forceinline__ void csr_piece(const DSeg& s, int64_t r, int q, int32_t& lo, int32_t& hi) {
+  const int32_t* pt = s.csr_ptab + r * s.csr_pt_stride;
+  lo = q == 0 ? __ldg(s.csr_lo + r) : __ldg(pt + q * s.csr_pt_step - 1);
+  hi = q == s.csr_np - 1 ? __ldg(s.csr_hi + r) : __ldg(pt + (q + 1) * s.csr_pt_step - 1);
+}
+
+// Root-sorted fold in the reference order (self leaves ascending, then remote
+// groups ascending rank, each in ascending leaf order), one thread per root
+// item: sequential per root, so floating-point results are bit-identical to
+// the CPU reference, and a warp instruction advances 32 roots at once.
+// With pieces (csr_np > 1) the grid walks L2-sized leaf windows piece-major
+// (see run_csr_warp).
 template <class T, int OP>
 __device__ __forceinline__ void run_csr(const DSeg& s, const LaunchParams& P, int64_t blk,
                                         bool fetch) {
@@ -282,80 +328,42 @@ __device__ __forceinline__ void run_csr(const DSeg& s, const LaunchParams& P, in
   const int64_t bl = P.bl;
   const int64_t total = s.n * bl;
   const ItemMap im{bl, total < (int64_t(1) << 31), P.bldiv};
-  const int64_t base = blk * (kThreads * kItems) + threadIdx.x;
-#pragma unroll 1
-  for (int u = 0; u < kItems; ++u) {
-    const int64_t e = base + static_cast<int64_t>(u) * kThreads;
-    if (e >= total) break;
+  const int64_t t0 = blk * kThreads + threadIdx.x;
+  if (s.csr_np <= 1) {
+    if (t0 >= total) return;
     int64_t r, k;
-    im.split(e, r, k);
+    im.split(t0, r, k);
     const int32_t lo = __ldg(s.csr_lo + r);
     const int32_t hi = __ldg(s.csr_hi + r);
-    if (lo >= hi) continue;
+    if (lo >= hi) return;
     const int64_t ro = static_cast<int64_t>(__ldg(s.csr_roots + r)) * bl + k;
-    T acc = root[ro];
-    int32_t j = lo;
-    // Batches of 4: issue the index and value loads before the dependent fold.
-    for (; j + 4 <= hi; j += 4) {
-      int32_t en[4];
-      T c[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) en[q] = __ldg(s.csr_ent + j + q);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        c[q] = en[q] >= 0 ? leaf[static_cast<int64_t>(en[q]) * bl + k]
-                          : stage[static_cast<int64_t>(-en[q] - 1) * bl + k];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (fetch) {
-          if (en[q] >= 0)
-            aux[static_cast<int64_t>(en[q]) * bl + k] = acc;
-          else
-            stage[static_cast<int64_t>(-en[q] - 1) * bl + k] = acc;
-        }
-        acc = apply_op<T, OP>(acc, c[q]);
-      }
+    root[ro] = csr_thread_range<T, OP>(s, leaf, stage, aux, bl, k, lo, hi, root[ro], fetch);
+    return;
+  }
+  for (int q = 0; q < s.csr_np; ++q) {
+    for (int64_t e = t0; e < total; e += s.csr_grid_threads) {
+      int64_t r, k;
+      im.split(e, r, k);
+      int32_t lo, hi;
+      csr_piece(s, r, q, lo, hi);
+      if (lo >= hi) continue;
+      const int64_t ro = static_cast<int64_t>(__ldg(s.csr_roots + r)) * bl + k;
+      root[ro] = csr_thread_range<T, OP>(s, leaf, stage, aux, bl, k, lo, hi, root[ro], fetch);
     }
-    for (; j < hi; ++j) {
-      const int32_t en = __ldg(s.csr_ent + j);
-      const T c = en >= 0 ? leaf[static_cast<int64_t>(en) * bl + k]
-                          : stage[static_cast<int64_t>(-en - 1) * bl + k];
-      if (fetch) {
-        if (en >= 0)
-          aux[static_cast<int64_t>(en) * bl + k] = acc;
-        else
-          stage[static_cast<int64_t>(-en - 1) * bl + k] = acc;
-      }
-      acc = apply_op<T, OP>(acc, c);
-    }
-    root[ro] = acc;
   }
 }
 
-// Warp-per-root CSR fold / fetch for high-degree roots. The 32 lanes load 32
-// consecutive contributions (coalesced entry reads); with csr_seq the fold
-// runs in exact entry order through shuffles (bit-identical to the sequential
-// reference for floating point), otherwise as a warp tree (fold) or inclusive
-// scan (fetch), exact for the associative integer ops.
+// One warp folds contributions [lo, hi) of one root item into acc (held by
+// every lane). The 32 lanes load 32 consecutive contributions (coalesced
+// entry reads), 8 chunks in flight; with csr_seq the fold runs in exact entry
+// order through shuffles (bit-identical to the sequential reference for
+// floating point), otherwise as a warp tree (fold) or inclusive scan (fetch),
+// exact for the associative integer ops.
 template <class T, int OP>
-__device__ __forceinline__ void run_csr_warp(const DSeg& s, const LaunchParams& P, int64_t blk,
-                                             bool fetch) {
-  T* root = static_cast<T*>(P.bufs[s.dst_buf]);
-  const T* leaf = static_cast<const T*>(P.bufs[s.src_buf]);
-  T* stage = static_cast<T*>(P.bufs[s.stage_buf]);
-  T* aux = static_cast<T*>(P.bufs[s.aux_buf]);
-  const int64_t bl = P.bl;
+__device__ __forceinline__ T csr_warp_range(const DSeg& s, const T* leaf, T* stage, T* aux,
+                                            int64_t bl, int64_t k, int32_t lo, int32_t hi, T acc,
+                                            bool fetch) {
   const int lane = threadIdx.x & 31;
-  const int64_t item = blk * (kThreads / 32) + (threadIdx.x >> 5);
-  if (item >= s.n * bl) return;
-  int64_t r, k;
-  const ItemMap im{bl, s.n * bl < (int64_t(1) << 31), P.bldiv};
-  im.split(item, r, k);
-  const int32_t lo = __ldg(s.csr_lo + r);
-  const int32_t hi = __ldg(s.csr_hi + r);
-  if (lo >= hi) return;
-  const int64_t ro = static_cast<int64_t>(__ldg(s.csr_roots + r)) * bl + k;
-  T acc = root[ro];
   constexpr int kChunks = 8;  // 256 contributions in flight per warp
   for (int32_t sbase = lo; sbase < hi; sbase += 32 * kChunks) {
     int32_t ens[kChunks];
@@ -375,45 +383,95 @@ __device__ __forceinline__ void run_csr_warp(const DSeg& s, const LaunchParams& 
     }
 #pragma unroll
     for (int c = 0; c < kChunks; ++c) {
-    const int32_t base = sbase + 32 * c;
-    if (base >= hi) break;
-    const int32_t j = base + lane;
-    const int cnt = min(32, hi - base);
-    const int32_t en = ens[c];
-    const T v = vs[c];
-    T mine = acc;
-    if (s.csr_seq) {
-      for (int q = 0; q < cnt; ++q) {
-        const T vq = __shfl_sync(0xffffffffu, v, q);
-        if (lane == q) mine = acc;
-        acc = apply_op<T, OP>(acc, vq);
+      const int32_t base = sbase + 32 * c;
+      if (base >= hi) break;
+      const int32_t j = base + lane;
+      const int cnt = min(32, hi - base);
+      const int32_t en = ens[c];
+      const T v = vs[c];
+      T mine = acc;
+      if (s.csr_seq) {
+        for (int q = 0; q < cnt; ++q) {
+          const T vq = __shfl_sync(0xffffffffu, v, q);
+          if (lane == q) mine = acc;
+          acc = apply_op<T, OP>(acc, vq);
+        }
+      } else if (!fetch) {
+        T x = v;
+        for (int off = 16; off > 0; off >>= 1) {
+          const T y = __shfl_down_sync(0xffffffffu, x, off);
+          if (lane + off < cnt) x = apply_op<T, OP>(x, y);
+        }
+        acc = apply_op<T, OP>(acc, __shfl_sync(0xffffffffu, x, 0));
+      } else {
+        T x = v;  // inclusive scan over lanes < cnt
+        for (int off = 1; off < 32; off <<= 1) {
+          const T y = __shfl_up_sync(0xffffffffu, x, off);
+          if (lane >= off && lane < cnt) x = apply_op<T, OP>(y, x);
+        }
+        const T excl = __shfl_up_sync(0xffffffffu, x, 1);
+        mine = lane == 0 ? acc : apply_op<T, OP>(acc, excl);
+        acc = apply_op<T, OP>(acc, __shfl_sync(0xffffffffu, x, cnt - 1));
       }
-    } else if (!fetch) {
-      T x = v;
-      for (int off = 16; off > 0; off >>= 1) {
-        const T y = __shfl_down_sync(0xffffffffu, x, off);
-        if (lane + off < cnt) x = apply_op<T, OP>(x, y);
+      if (fetch && j < hi) {
+        if (en >= 0)
+          aux[static_cast<int64_t>(en) * bl + k] = mine;
+        else
+          stage[static_cast<int64_t>(-en - 1) * bl + k] = mine;
       }
-      acc = apply_op<T, OP>(acc, __shfl_sync(0xffffffffu, x, 0));
-    } else {
-      T x = v;  // inclusive scan over lanes < cnt
-      for (int off = 1; off < 32; off <<= 1) {
-        const T y = __shfl_up_sync(0xffffffffu, x, off);
-        if (lane >= off && lane < cnt) x = apply_op<T, OP>(y, x);
-      }
-      const T excl = __shfl_up_sync(0xffffffffu, x, 1);
-      mine = lane == 0 ? acc : apply_op<T, OP>(acc, excl);
-      acc = apply_op<T, OP>(acc, __shfl_sync(0xffffffffu, x, cnt - 1));
-    }
-    if (fetch && j < hi) {
-      if (en >= 0)
-        aux[static_cast<int64_t>(en) * bl + k] = mine;
-      else
-        stage[static_cast<int64_t>(-en - 1) * bl + k] = mine;
-    }
     }
   }
-  if (lane == 0) root[ro] = acc;
+  return acc;
+}
+
+// Warp-per-root CSR fold / fetch for high-degree roots.
+//
+// L2-tiled ("pieces") when the gathered leaf array is larger than L2: the
+// self contributions of every root are split at leaf-index boundaries
+// (csr_ptab), and the grid — sized to be fully resident — walks the pieces
+// in order, each warp folding piece q of all its roots before piece q+1, so
+// at any time the CTAs gather from one L2-sized window of the leaf (and
+// leafupdate) arrays and every 32-byte sector is fetched from DRAM once
+// instead of once per contribution. Each root is owned by one warp, so the
+// fold order per root is unchanged (pieces ascend in leaf index, exactly the
+// reference order) and no grid barrier is needed for correctness.
+template <class T, int OP>
+__device__ __forceinline__ void run_csr_warp(const DSeg& s, const LaunchParams& P, int64_t blk,
+                                             bool fetch) {
+  T* root = static_cast<T*>(P.bufs[s.dst_buf]);
+  const T* leaf = static_cast<const T*>(P.bufs[s.src_buf]);
+  T* stage = static_cast<T*>(P.bufs[s.stage_buf]);
+  T* aux = static_cast<T*>(P.bufs[s.aux_buf]);
+  const int64_t bl = P.bl;
+  const int lane = threadIdx.x & 31;
+  const int64_t items = s.n * bl;
+  const ItemMap im{bl, items < (int64_t(1) << 31), P.bldiv};
+  const int64_t w0 = blk * (kThreads / 32) + (threadIdx.x >> 5);
+  if (s.csr_np <= 1) {
+    if (w0 >= items) return;
+    int64_t r, k;
+    im.split(w0, r, k);
+    const int32_t lo = __ldg(s.csr_lo + r);
+    const int32_t hi = __ldg(s.csr_hi + r);
+    if (lo >= hi) return;
+    const int64_t ro = static_cast<int64_t>(__ldg(s.csr_roots + r)) * bl + k;
+    const T acc = csr_warp_range<T, OP>(s, leaf, stage, aux, bl, k, lo, hi, root[ro], fetch);
+    if (lane == 0) root[ro] = acc;
+    return;
+  }
+  const int64_t nw = s.csr_grid_threads / 32;
+  for (int q = 0; q < s.csr_np; ++q) {
+    for (int64_t w = w0; w < items; w += nw) {
+      int64_t r, k;
+      im.split(w, r, k);
+      int32_t lo, hi;
+      csr_piece(s, r, q, lo, hi);
+      if (lo >= hi) continue;
+      const int64_t ro = static_cast<int64_t>(__ldg(s.csr_roots + r)) * bl + k;
+      const T acc = csr_warp_range<T, OP>(s, leaf, stage, aux, bl, k, lo, hi, root[ro], fetch);
+      if (lane == 0) root[ro] = acc;
+    }
+  }
 }
 
 // Free-order fetch-and-op: fetched = atomic(root[dpat(i)] op= src[spat(i)]),
@@ -449,6 +507,79 @@ __device__ __forceinline__ void run_atomic_fetch(const DSeg& s, const LaunchPara
   }
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Thread 0 acquires every selected flag (system scope: written by a peer GPU
+// over NVLink), then the CTA proceeds. A peer that never signals (it died or
+// broke the collective order) ends in a trap after 30 s, not a hang.
+__device__ __forceinline__ void wait_flags(const LaunchParams& P, uint32_t mask) {
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = global_ns();
+    for (uint32_t m = mask; m; m &= m - 1) {
+      const FlagWait& w = P.waits[__ffs(m) - 1];
+      const unsigned long long need = *w.count + w.delta;
+      while (ld_acquire_sys(w.flag) < need) {
+        __nanosleep(32);
+        if (global_ns() - t0 > 30000000000ull) {
+          printf("sfgpu p2p: peer flag stuck at %llu < %llu\n", ld_acquire_sys(w.flag), need);
+          __trap();
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Launch completion: the last CTA raises every done flag (after all CTAs'
+// reads of the slot and stores are fenced).
+__device__ __forceinline__ void signal_launch_done(const LaunchParams& P) {
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  const unsigned int prev = atomicAdd(P.done_count, 1u);
+  if (prev + 1 == gridDim.x) {
+    *P.done_count = 0u;
+    __threadfence_system();
+    for (int i = 0; i < P.ndone; ++i) {
+      const unsigned long long v = *P.done_seq[i] + 1;
+      *P.done_seq[i] = v;
+      st_release_sys(P.done_flag[i], v);
+    }
+  }
+}
+
+// Put completion: every CTA of the segment fences its stores (peer stores
+// over NVLink included) at system scope and counts itself in; the last one
+// publishes the segment's flag with a system-scope release store, which the
+// receiving GPU's stream waits on (cuStreamWaitValue64, ops.cpp).
+__device__ __forceinline__ void signal_segment_done(const DSeg& seg, int64_t nblk) {
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  const unsigned int prev = atomicAdd(seg.sig_count, 1u);
+  if (static_cast<int64_t>(prev) + 1 == nblk) {
+    *seg.sig_count = 0u;  // ready for the next launch on this stream
+    __threadfence_system();
+    const unsigned long long v = *seg.sig_seq + 1;
+    *seg.sig_seq = v;
+    st_release_sys(seg.sig_flag, v);
+  }
+}
+
 // FULL = the launch contains root-sorted (CSR) or fetch segments. Pair-only
 // launches (every pack, unpack and structured local scatter) get their own
 // instantiation so the CSR paths do not raise their register allocation.
@@ -459,6 +590,7 @@ __global__ void __launch_bounds__(kThreads) segments_kernel(const __grid_constan
   while (s + 1 < P.nseg && b >= P.block_start[s + 1]) ++s;
   const DSeg& seg = P.seg[s];
   const int64_t blk = b - P.block_start[s];
+  if (seg.wait_mask) wait_flags(P, seg.wait_mask);
   switch (seg.type) {
     case SEG_PAIR:
       if (seg.run > 0) {
@@ -503,6 +635,8 @@ __global__ void __launch_bounds__(kThreads) segments_kernel(const __grid_constan
     default:
       break;
   }
+  if (seg.sig_flag != nullptr) signal_segment_done(seg, P.block_start[s + 1] - P.block_start[s]);
+  if (P.ndone > 0) signal_launch_done(P);
 }
 
 template <class T, int OP>
@@ -565,6 +699,49 @@ __global__ void digest_kernel(const unsigned char* p, size_t bytes, unsigned lon
   if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
 
+template <class T, int OP>
+int64_t resident_full() {
+  static const int64_t v = [] {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, segments_kernel<T, OP, true>, kThreads, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return static_cast<int64_t>(std::max(1, per_sm) * std::max(1, sms));
+  }();
+  return v;
+}
+
+template <class T>
+int64_t resident_t(int op) {
+  switch (op) {
+    case OP_SUM: return resident_full<T, OP_SUM>();
+    case OP_PROD: return resident_full<T, OP_PROD>();
+    case OP_MAX: return resident_full<T, OP_MAX>();
+    case OP_MIN: return resident_full<T, OP_MIN>();
+    default: break;
+  }
+  if constexpr (std::is_integral_v<T>) {
+    switch (op) {
+      case OP_LAND: return resident_full<T, OP_LAND>();
+      case OP_LOR: return resident_full<T, OP_LOR>();
+      case OP_BAND: return resident_full<T, OP_BAND>();
+      case OP_BOR: return resident_full<T, OP_BOR>();
+      default: break;
+    }
+  }
+  return 148;
+}
+
+// CTAs of the FULL (CSR-capable) instantiation that fit on the GPU at once.
+int64_t resident_ctas(ElemType t, int op) {
+  switch (t) {
+    case ElemType::i32: return resident_t<int32_t>(op);
+    case ElemType::i64: return resident_t<int64_t>(op);
+    case ElemType::f64: return resident_t<double>(op);
+    default: return 148;
+  }
+}
+
 }  // namespace
 
 int launch_segments(LaunchParams& p, ElemType t, int op, cudaStream_t stream) {
@@ -575,8 +752,15 @@ int launch_segments(LaunchParams& p, ElemType t, int op, cudaStream_t stream) {
     if (items <= 0) continue;
     p.seg[n] = p.seg[s];
     p.block_start[n] = blocks;
-    const int64_t per_block = p.seg[s].csr_warp ? kThreads / 32 : kThreads * kItems;
-    blocks += (items + per_block - 1) / per_block;
+    const bool csr = p.seg[s].type == SEG_CSR_FOLD || p.seg[s].type == SEG_CSR_FETCH;
+    const int64_t per_block = !csr ? kThreads * kItems : p.seg[s].csr_warp ? kThreads / 32 : kThreads;
+    int64_t nb = (items + per_block - 1) / per_block;
+    if (csr && p.seg[s].csr_np > 1) {
+      // Piece-major walk: every CTA of the segment must be resident at once.
+      nb = std::min<int64_t>(nb, resident_ctas(t, op));
+      p.seg[n].csr_grid_threads = nb * kThreads;
+    }
+    blocks += nb;
     ++n;
   }
   p.nseg = n;

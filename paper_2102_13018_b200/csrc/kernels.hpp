@@ -68,8 +68,10 @@ enum BufId : int32_t {
   BUF_LEAFUPDATE = 4,  // fetch-and-op leafupdate
   BUF_LEAF_REPLY = 5,  // fetch-and-op reply staging on the leaf side
   BUF_SRC_RO = 6,      // read-only source alias (leafdata for reduce/fetch)
-  BUF_COUNT = 8
+  BUF_PEER0 = 8,       // p2p transport: peer r's mapped staging slot is BUF_PEER0 + r
+  BUF_COUNT = 8 + 16
 };
+constexpr int kMaxPeers = BUF_COUNT - BUF_PEER0;
 
 struct DSeg {
   DPat src;
@@ -98,6 +100,36 @@ struct DSeg {
   // with a warp tree/scan, which is bit-identical for them.
   int32_t csr_warp = 0;
   int32_t csr_seq = 1;
+  // L2-tiled CSR: csr_np > 1 pieces, walked piece-major by a resident grid
+  // of csr_grid_threads threads (set at launch). Piece q of root r spans
+  // entries [b(q), b(q+1)) with b(0) = csr_lo[r], b(np) = csr_hi[r] and
+  // b(q) = csr_ptab[r * csr_pt_stride + q * csr_pt_step - 1] in between.
+  int32_t csr_np = 1;
+  int32_t csr_pt_stride = 0;
+  int32_t csr_pt_step = 1;
+  const int32_t* csr_ptab = nullptr;
+  int64_t csr_grid_threads = 0;
+  // One-sided put/signal (p2p backend, the paper's put + signal,
+  // PAPER.md:904-922). Before touching data, every CTA of the segment waits
+  // until each flag of LaunchParams::waits selected by wait_mask reaches its
+  // target (a peer's "slot free" for puts, a peer's "data arrived" for
+  // unpacks). After its last CTA has stored its part (stores into a peer's
+  // mapped slot over NVLink), the segment advances its message counter
+  // *sig_seq and publishes the new count in *sig_flag with a system-scope
+  // release; sig_count is a local CTA arrival counter the last CTA resets.
+  // Counters live in device memory, so a captured CUDA graph replays the
+  // protocol correctly.
+  uint32_t wait_mask = 0;
+  unsigned int* sig_count = nullptr;
+  unsigned long long* sig_flag = nullptr;
+  unsigned long long* sig_seq = nullptr;
+};
+
+// Wait until *flag >= *count + delta (count: a local message counter).
+struct FlagWait {
+  const unsigned long long* flag = nullptr;
+  const unsigned long long* count = nullptr;
+  unsigned long long delta = 0;
 };
 
 constexpr int kMaxSegs = 12;
@@ -112,6 +144,15 @@ struct LaunchParams {
   FastDiv bldiv;
   int nseg = 0;
   int vec_ok = 0;  // reserved
+  // p2p: flags segments wait on (bit i of DSeg::wait_mask = waits[i]) and the
+  // acknowledgements the launch raises once all its CTAs are done (advance
+  // the local counter *done_seq[i], publish it in a peer's "slot free" flag
+  // done_flag[i]); done_count is a local CTA arrival counter.
+  FlagWait waits[kMaxPeers];
+  unsigned long long* done_flag[kMaxPeers];
+  unsigned long long* done_seq[kMaxPeers];
+  int ndone = 0;
+  unsigned int* done_count = nullptr;
 };
 
 // Element type the kernel instantiates for.

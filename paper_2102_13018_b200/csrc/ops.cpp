@@ -20,6 +20,8 @@
 // ascending leaf index (ops.cpp:364,372-376; oracle.cpp:84-90) — so
 // floating-point results are bit-identical to the CPU reference. The
 // free-order mode uses atomics (pack.cpp:47-58 "atomics" mode).
+#include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -74,7 +76,7 @@ enum class CsrRange { self_only, remote_only, all };
 
 // seq: keep the exact sequential fold order inside a warp (float data in
 // deterministic mode). High-degree roots get a warp each.
-DSeg csr_seg(const DevPlan& d, CsrRange range, int32_t type, bool seq) {
+DSeg csr_seg(const DevPlan& d, CsrRange range, int32_t type, bool seq, size_t ub) {
   DSeg s;
   s.type = type;
   const int64_t entries = range == CsrRange::self_only ? d.csr_self_entries
@@ -106,6 +108,26 @@ DSeg csr_seg(const DevPlan& d, CsrRange range, int32_t type, bool seq) {
       s.csr_lo = d.csr_off;
       s.csr_hi = d.csr_off + 1;
       break;
+  }
+  // L2 tiling: pieces of the leaf (and, for fetch, leafupdate) arrays that
+  // together fit a ~40 MB window of the 126 MB L2.
+  static const bool no_pieces = std::getenv("SFG_NO_L2_PIECES") != nullptr;
+  if (range != CsrRange::remote_only && d.csr_ptab && d.csr_np_max > 1 && !no_pieces) {
+    const double window = 40e6;
+    const double per_piece = static_cast<double>(ub) * static_cast<double>(d.csr_piece_leaves) *
+                             (type == SEG_CSR_FETCH ? 2.0 : 1.0);
+    const int step = std::max(1, static_cast<int>(window / per_piece));
+    const int np = (d.csr_np_max + step - 1) / step;
+    if (np > 1) {
+      s.csr_np = np;
+      s.csr_pt_stride = d.csr_np_max - 1;
+      s.csr_pt_step = step;
+      s.csr_ptab = d.csr_ptab;
+      // Enough roots to fill the GPU with one thread each: a thread per root
+      // folds sequentially with 8 loads in flight and no shuffles (32 roots
+      // per warp instruction instead of one contribution).
+      if (s.n >= 16384) s.csr_warp = 0;
+    }
   }
   return s;
 }
@@ -175,7 +197,9 @@ struct Launch {
     counters().kernel_launches += static_cast<uint64_t>(launched);
     if (timed) {
       SFG_CUDA(cudaEventRecord(e1, st));
-      timing_record(tag, e0, e1, algorithmic_bytes(u));
+      double link = 0;
+      for (int s = 0; s < p.nseg; ++s) link += remote_put[s] ? static_cast<double>(p.seg[s].n) * u.bytes() : 0.0;
+      timing_record(tag, e0, e1, algorithmic_bytes(u), link);
     }
   }
 
@@ -206,7 +230,45 @@ struct Launch {
     return b;
   }
 
+  // p2p: wait until *flag >= *count + delta; returns the segment mask bit.
+  uint32_t add_wait(const unsigned long long* flag, const unsigned long long* count, uint64_t delta) {
+    SFG_REQUIRE(nwait < kMaxPeers, "p2p: too many flag waits in one launch");
+    p.waits[nwait].flag = flag;
+    p.waits[nwait].count = count;
+    p.waits[nwait].delta = delta;
+    return 1u << nwait++;
+  }
+
+  // p2p: once every CTA of the launch is done, ++*seq and publish it in flag.
+  void add_done(unsigned long long* flag, unsigned long long* seq, unsigned int* counter) {
+    SFG_REQUIRE(p.ndone < kMaxPeers, "p2p: too many completion flags in one launch");
+    p.done_flag[p.ndone] = flag;
+    p.done_seq[p.ndone] = seq;
+    p.done_count = counter;
+    ++p.ndone;
+  }
+
+  // One-sided put into a peer's slot (p2p): the segment's destination is
+  // buffer `BUF_PEER0 + k` = `base`; it waits for `wait_mask`, and its
+  // completion advances *seq and publishes it in `flag`.
+  void add_put(const DPat& src, int sbuf, int k, void* base, int64_t peer_off, int64_t n,
+               uint32_t wait_mask, unsigned int* counters, unsigned long long* flag,
+               unsigned long long* seq, bool remote, int64_t src_distinct = -1) {
+    SFG_REQUIRE(k < kMaxPeers, "p2p: too many neighbor groups in one launch");
+    DSeg s = pair_seg(src, sbuf, contig(peer_off), BUF_PEER0 + k, n, true);
+    s.wait_mask = wait_mask;
+    s.sig_count = counters + k;
+    s.sig_flag = flag;
+    s.sig_seq = seq;
+    p.bufs[BUF_PEER0 + k] = base;
+    remote_put[p.nseg] = remote;
+    add(s, 0, src_distinct);
+  }
+
+  int nwait = 0;
+
   const char* tag = "kernel";
+  bool remote_put[kMaxSegs] = {};
   int64_t csr_entries[kMaxSegs] = {};
   int64_t distinct_src[kMaxSegs] = {};
   int64_t distinct_dst[kMaxSegs] = {};
@@ -330,7 +392,24 @@ void begin_phase(OpHandle& h, Launch& pack, Launch& local, const std::vector<Xfe
     local.tag = tag_of(h, 3);
   }
   pack.run(h.unit, h.op, cs);
+  const bool timed = timing_enabled();
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timed) {
+    e0 = timing_event();
+    e1 = timing_event();
+    SFG_CUDA(cudaEventRecord(e0, cs));
+  }
   c.transport().start(tag, sends, recvs, cs);
+  if (timed) {
+    // Exchange interval on the comm stream (includes the rendezvous with the
+    // peers); link bytes = what this rank sends to other ranks.
+    SFG_CUDA(cudaEventRecord(e1, cs));
+    double link = 0;
+    for (const auto& s : sends)
+      if (s.peer != c.rank()) link += static_cast<double>(s.bytes);
+    static const char* xt[5] = {"bcast_xfer", "reduce_xfer", "fetch_xfer", "gather_xfer", "scatter_xfer"};
+    timing_record(xt[static_cast<int>(h.kind)], e0, e1, 0.0, link);
+  }
   counters().transport_calls++;
   if (!fuse) local.run(h.unit, h.op, h.stream);
 }
@@ -342,6 +421,96 @@ void end_wait(OpHandle& h, uint64_t tag, const std::vector<XferOp>& recvs) {
   c.join(h.stream);
 }
 
+// ------------------------------------------------- one-sided (p2p) phases
+//
+// Message counts per directed pair (Staging) replace the reference's
+// SendSig/RecvSig clearing (ops.cpp:160-246): the n-th put from me into d's
+// slot waits in-kernel for d.free[me] >= n-1 and raises d.arrive[me] = n;
+// the unpack of the n-th message from s waits for arrive[s] >= n and its
+// launch raises s.free[me] = n when done. With a small (fused) local part
+// the whole operation is two launches on the caller's stream; a large local
+// scatter runs on the caller's stream while the puts run on the comm stream.
+bool use_p2p(const OpHandle& h) { return h.sf->comm().p2p() && h.stg && h.stg->flags; }
+
+void p2p_begin(OpHandle& h, Launch& pack, Launch& local) {
+  Comm& c = h.sf->comm();
+  h.xfer = pack.p.nseg > 0;
+  const bool fuse = !h.xfer || local.algorithmic_bytes(h.unit) < kFuseLocalBytes;
+  if (fuse) {
+    for (int i = 0; i < local.p.nseg; ++i)
+      pack.add(local.p.seg[i], local.csr_entries[i], local.distinct_src[i], local.distinct_dst[i]);
+    pack.tag = tag_of(h, 0);
+    pack.run(h.unit, h.op, h.stream);
+    h.forked = false;
+  } else {
+    cudaStream_t cs = c.comm_stream();
+    c.fork(h.stream);
+    pack.tag = tag_of(h, 2);
+    local.tag = tag_of(h, 3);
+    pack.run(h.unit, h.op, cs);
+    local.run(h.unit, h.op, h.stream);
+    h.forked = true;
+  }
+  if (h.xfer) counters().transport_calls++;
+}
+
+// Before the unpack: order the caller's stream after this rank's own puts
+// (they read the caller's buffers, and a spinning unpack must never starve
+// them of SMs).
+void p2p_join(OpHandle& h) {
+  if (h.forked) h.sf->comm().join(h.stream);
+  h.forked = false;
+}
+
+// Puts of `groups` from buffer `sbuf` (each group's own pattern, or its
+// staging range when !use_pat) into each peer's stage `region` (0 leaf,
+// 1 root, 2 reply).
+void add_puts(OpHandle& h, Launch& L, const std::vector<DevPlan::Seg>& groups, bool use_pat,
+              int sbuf, int region) {
+  Staging& s = *h.stg;
+  const int me = h.sf->comm().rank();
+  const size_t ub = h.unit.bytes();
+  for (size_t k = 0; k < groups.size(); ++k) {
+    const auto& g = groups[k];
+    const PeerSlot& ps = s.peers[static_cast<size_t>(g.rank)];
+    char* base = ps.base + (region == 0 ? 0 : region == 1 ? ps.root_at : ps.reply_at);
+    const int64_t off = region == 1 ? ps.root_off : ps.leaf_off;
+    SFG_REQUIRE(off >= 0, "p2p: peer slot has no group for this rank");
+    // my previous messages into this region of g.rank consumed
+    const uint32_t wm = L.add_wait(s.free_flag(region, g.rank), s.sent(region, g.rank), 0);
+    L.add_put(use_pat ? g.pat : contig(g.stage_off), sbuf, static_cast<int>(k), base, off, g.n, wm,
+              s.seg_counts, s.peer_arrive_flag(region, g.rank, me), s.sent(region, g.rank),
+              g.rank != me, use_pat ? g.distinct : -1);
+    if (g.rank != me) counters().bytes_sent += static_cast<uint64_t>(g.n) * ub;
+    counters().pack_copies++;
+  }
+}
+
+// The next message from each group's rank: returns the wait bit per group
+// (in group order) and, when `ack` is set, makes the launch acknowledge the
+// messages (sender's free flag) once it is done.
+std::vector<uint32_t> add_receives(OpHandle& h, Launch& L, const std::vector<DevPlan::Seg>& groups,
+                                   int region, bool ack) {
+  Staging& s = *h.stg;
+  const int me = h.sf->comm().rank();
+  std::vector<uint32_t> bits;
+  for (const auto& g : groups) {
+    // the next message from g.rank arrived: arrive >= recvd + 1
+    bits.push_back(L.add_wait(s.arrive_flag(region, g.rank), s.recvd(region, g.rank), 1));
+    if (ack) L.add_done(s.peer_free_flag(region, g.rank, me), s.recvd(region, g.rank), s.done_count);
+    counters().bytes_recv += static_cast<uint64_t>(g.n) * h.unit.bytes();
+  }
+  return bits;
+}
+
+// Acknowledge the latest message from each group's rank in launch L.
+void add_acks(OpHandle& h, Launch& L, const std::vector<DevPlan::Seg>& groups, int region) {
+  Staging& s = *h.stg;
+  const int me = h.sf->comm().rank();
+  for (const auto& g : groups)
+    L.add_done(s.peer_free_flag(region, g.rank, me), s.recvd(region, g.rank), s.done_count);
+}
+
 // ---------------------------------------------------------- root -> leaf
 void begin_root_to_leaf(OpHandle& h) {
   StarForest& sf = *h.sf;
@@ -351,6 +520,14 @@ void begin_root_to_leaf(OpHandle& h) {
   Launch pack, local;
   set_bufs(pack, h, const_cast<void*>(h.src), h.dst, h.src);
   set_bufs(local, h, const_cast<void*>(h.src), h.dst, h.src);
+  if (use_p2p(h)) {
+    add_puts(h, pack, d.lg, true, BUF_ROOT, 0);
+    if (d.has_self)
+      local.add(pair_seg(d.self_root, BUF_ROOT, d.self_leaf, BUF_LEAF, d.n_self, replace), 0,
+                d.self_root_distinct);
+    p2p_begin(h, pack, local);
+    return;
+  }
 
   std::vector<XferOp> sends;
   for (const auto& g : d.lg) {
@@ -383,10 +560,23 @@ void end_root_to_leaf(OpHandle& h) {
   StarForest& sf = *h.sf;
   DevPlan& d = sf.dev();
   const bool replace = h.op == ReduceOp::replace;
-  end_wait(h, data_tag(h.opid), h.recvs);
   Launch L;
   L.tag = tag_of(h, 1);
   set_bufs(L, h, const_cast<void*>(h.src), h.dst, h.src);
+  if (use_p2p(h)) {
+    p2p_join(h);
+    const auto bits = add_receives(h, L, d.rg, 0, true);
+    for (size_t k = 0; k < d.rg.size(); ++k) {
+      const auto& g = d.rg[k];
+      DSeg s = pair_seg(contig(g.stage_off), BUF_LEAF_STAGE, g.pat, BUF_LEAF, g.n, replace);
+      s.wait_mask = bits[k];
+      L.add(s);
+      counters().unpack_copies++;
+    }
+    L.run(h.unit, h.op, h.stream);
+    return;
+  }
+  end_wait(h, data_tag(h.opid), h.recvs);
   for (size_t k = 0; k < d.rg.size(); ++k) {
     if (h.zero_copy_recv[k]) continue;
     const auto& g = d.rg[k];
@@ -406,16 +596,21 @@ void begin_leaf_to_root(OpHandle& h) {
   Launch pack, local;
   set_bufs(pack, h, h.dst, const_cast<void*>(h.src), h.src);
   set_bufs(local, h, h.dst, const_cast<void*>(h.src), h.src);
+  const bool p2p = use_p2p(h);
 
   std::vector<XferOp> sends;
-  for (const auto& g : d.rg) {
-    if (g.contiguous) {
-      sends.push_back({g.rank, const_cast<void*>(at(h.src, g.contig_start, ub)), static_cast<size_t>(g.n) * ub});
-      counters().pack_elided++;
-    } else {
-      pack.add(pair_seg(g.pat, BUF_LEAF, contig(g.stage_off), BUF_LEAF_STAGE, g.n, true));
-      sends.push_back({g.rank, at(h.stg->leaf_stage, g.stage_off, ub), static_cast<size_t>(g.n) * ub});
-      counters().pack_copies++;
+  if (p2p) {
+    add_puts(h, pack, d.rg, true, BUF_LEAF, 1);
+  } else {
+    for (const auto& g : d.rg) {
+      if (g.contiguous) {
+        sends.push_back({g.rank, const_cast<void*>(at(h.src, g.contig_start, ub)), static_cast<size_t>(g.n) * ub});
+        counters().pack_elided++;
+      } else {
+        pack.add(pair_seg(g.pat, BUF_LEAF, contig(g.stage_off), BUF_LEAF_STAGE, g.n, true));
+        sends.push_back({g.rank, at(h.stg->leaf_stage, g.stage_off, ub), static_cast<size_t>(g.n) * ub});
+        counters().pack_copies++;
+      }
     }
   }
   if (d.has_self) {
@@ -424,11 +619,15 @@ void begin_leaf_to_root(OpHandle& h) {
       local.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, replace), 0, -1,
                 d.self_root_distinct);
     } else if (prefer_csr(sf, det, CsrRange::self_only)) {
-      local.add(csr_seg(d, CsrRange::self_only, SEG_CSR_FOLD, exact_seq(h, det)), d.csr_self_entries);
+      local.add(csr_seg(d, CsrRange::self_only, SEG_CSR_FOLD, exact_seq(h, det), h.unit.bytes()), d.csr_self_entries);
     } else {
       local.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, false, true), 0, -1,
                 d.self_root_distinct);
     }
+  }
+  if (p2p) {
+    p2p_begin(h, pack, local);
+    return;
   }
 
   h.recvs.clear();
@@ -448,29 +647,39 @@ void end_leaf_to_root(OpHandle& h) {
   DevPlan& d = sf.dev();
   const bool replace = h.op == ReduceOp::replace;
   const bool det = sf.comm().config().deterministic;
-  end_wait(h, data_tag(h.opid), h.recvs);
   Launch L;
   L.tag = tag_of(h, 1);
   set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
+  std::vector<uint32_t> bits(d.lg.size(), 0);
+  if (use_p2p(h)) {
+    p2p_join(h);
+    bits = add_receives(h, L, d.lg, 1, true);
+  } else {
+    end_wait(h, data_tag(h.opid), h.recvs);
+  }
   if (!d.lg.empty()) {
     if (replace || !d.remote_root_dups) {
       if (replace && d.remote_root_dups) counters().replace_dup_collisions++;
       for (size_t k = 0; k < d.lg.size(); ++k) {
-        if (h.zero_copy_recv[k]) continue;
+        if (!h.zero_copy_recv.empty() && h.zero_copy_recv[k]) continue;
         const auto& g = d.lg[k];
-        L.add(pair_seg(contig(g.stage_off), BUF_ROOT_STAGE, g.pat, BUF_ROOT, g.n, replace), 0, -1,
-              g.distinct);
+        DSeg s = pair_seg(contig(g.stage_off), BUF_ROOT_STAGE, g.pat, BUF_ROOT, g.n, replace);
+        s.wait_mask = bits[k];
+        L.add(s, 0, -1, g.distinct);
         counters().unpack_copies++;
       }
     } else if (prefer_csr(sf, det, CsrRange::remote_only)) {
       // Ascending-rank fold of every remote contribution (ops.cpp:372-376).
-      L.add(csr_seg(d, CsrRange::remote_only, SEG_CSR_FOLD, exact_seq(h, det)),
-            d.csr_remote_entries);
+      DSeg s = csr_seg(d, CsrRange::remote_only, SEG_CSR_FOLD, exact_seq(h, det), h.unit.bytes());
+      for (uint32_t b : bits) s.wait_mask |= b;
+      L.add(s, d.csr_remote_entries);
       counters().unpack_copies += d.lg.size();
     } else {
-      for (const auto& g : d.lg) {
-        L.add(pair_seg(contig(g.stage_off), BUF_ROOT_STAGE, g.pat, BUF_ROOT, g.n, false, true), 0, -1,
-              g.distinct);
+      for (size_t k = 0; k < d.lg.size(); ++k) {
+        const auto& g = d.lg[k];
+        DSeg s = pair_seg(contig(g.stage_off), BUF_ROOT_STAGE, g.pat, BUF_ROOT, g.n, false, true);
+        s.wait_mask = bits[k];
+        L.add(s, 0, -1, g.distinct);
         counters().unpack_copies++;
       }
     }
@@ -485,6 +694,11 @@ void begin_fetch(OpHandle& h) {
   const size_t ub = h.unit.bytes();
   Launch pack, local;
   set_bufs(pack, h, h.dst, const_cast<void*>(h.src), h.src);
+  if (use_p2p(h)) {
+    add_puts(h, pack, d.rg, true, BUF_LEAF, 1);
+    p2p_begin(h, pack, local);
+    return;
+  }
   std::vector<XferOp> sends;
   for (const auto& g : d.rg) {
     if (g.contiguous) {
@@ -508,36 +722,67 @@ void end_fetch(OpHandle& h) {
   Comm& c = sf.comm();
   const size_t ub = h.unit.bytes();
   const bool det = c.config().deterministic;
-  end_wait(h, data_tag(h.opid), h.recvs);
+  const bool p2p = use_p2p(h);
+  Launch L;
+  L.tag = "fetch_end";
+  set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
+  std::vector<uint32_t> bits(d.lg.size(), 0);
+  if (p2p) {
+    p2p_join(h);
+    // Consumed (acknowledged) only after the replies have been read out of
+    // the root stage below.
+    bits = add_receives(h, L, d.lg, 1, false);
+  } else {
+    end_wait(h, data_tag(h.opid), h.recvs);
+  }
   if (!d.rg.empty() && h.stg->leaf_reply == nullptr && h.stg->leaf_bytes)
     SFG_CUDA(cudaMalloc(&h.stg->leaf_reply, h.stg->leaf_bytes));
 
   // Root side: serialize every contribution per root.
-  {
-    Launch L;
-    L.tag = "fetch_end";
-    set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
-    if (prefer_csr(sf, det, CsrRange::all)) {
-      L.add(csr_seg(d, CsrRange::all, SEG_CSR_FETCH, exact_seq(h, det)),
-            d.csr_self_entries + d.csr_remote_entries);
-    } else {
-      if (d.has_self) {
-        DSeg s = pair_seg(d.self_leaf, BUF_SRC_RO, d.self_root, BUF_ROOT, d.n_self, false);
-        s.type = SEG_ATOMIC_FETCH;
-        s.aux_buf = BUF_LEAFUPDATE;
-        L.add(s);
-      }
-      for (const auto& g : d.lg) {
-        DSeg s = pair_seg(contig(g.stage_off), BUF_ROOT_STAGE, g.pat, BUF_ROOT, g.n, false);
-        s.type = SEG_ATOMIC_FETCH;
-        s.aux_buf = BUF_ROOT_STAGE;
-        L.add(s);
-      }
+  if (prefer_csr(sf, det, CsrRange::all)) {
+    DSeg s = csr_seg(d, CsrRange::all, SEG_CSR_FETCH, exact_seq(h, det), h.unit.bytes());
+    for (uint32_t b : bits) s.wait_mask |= b;
+    L.add(s, d.csr_self_entries + d.csr_remote_entries);
+  } else {
+    if (d.has_self) {
+      DSeg s = pair_seg(d.self_leaf, BUF_SRC_RO, d.self_root, BUF_ROOT, d.n_self, false);
+      s.type = SEG_ATOMIC_FETCH;
+      s.aux_buf = BUF_LEAFUPDATE;
+      L.add(s);
     }
-    L.run(h.unit, h.op, h.stream);
+    for (size_t k = 0; k < d.lg.size(); ++k) {
+      const auto& g = d.lg[k];
+      DSeg s = pair_seg(contig(g.stage_off), BUF_ROOT_STAGE, g.pat, BUF_ROOT, g.n, false);
+      s.type = SEG_ATOMIC_FETCH;
+      s.aux_buf = BUF_ROOT_STAGE;
+      s.wait_mask = bits[k];
+      L.add(s);
+    }
   }
+  L.run(h.unit, h.op, h.stream);
 
   // Replies travel back in place (ops.cpp:559-561), then land in leafupdate.
+  if (p2p) {
+    Launch R;
+    R.tag = "fetch_replies";
+    set_bufs(R, h, h.dst, const_cast<void*>(h.src), h.src);
+    add_puts(h, R, d.lg, false, BUF_ROOT_STAGE, 2);
+    add_acks(h, R, d.lg, 1);
+    R.run(h.unit, ReduceOp::replace, h.stream);
+    Launch U;
+    U.tag = "fetch_end_replies";
+    set_bufs(U, h, h.dst, const_cast<void*>(h.src), h.src);
+    const auto rbits = add_receives(h, U, d.rg, 2, true);
+    for (size_t k = 0; k < d.rg.size(); ++k) {
+      const auto& g = d.rg[k];
+      DSeg s = pair_seg(contig(g.stage_off), BUF_LEAF_REPLY, g.pat, BUF_LEAFUPDATE, g.n, true);
+      s.wait_mask = rbits[k];
+      U.add(s);
+      counters().unpack_copies++;
+    }
+    U.run(h.unit, ReduceOp::replace, h.stream);
+    return;
+  }
   std::vector<XferOp> sends;
   for (const auto& g : d.lg)
     sends.push_back({g.rank, at(h.stg->root_stage, g.stage_off, ub), static_cast<size_t>(g.n) * ub});

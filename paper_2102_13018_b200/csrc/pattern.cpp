@@ -113,6 +113,7 @@ struct TimingState {
     std::string tag;
     cudaEvent_t a, b;
     double bytes;
+    double link_bytes;
   };
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> pool;
@@ -144,9 +145,10 @@ cudaEvent_t timing_event() {
   return e;
 }
 
-void timing_record(const char* tag, cudaEvent_t a, cudaEvent_t b, double bytes) {
+void timing_record(const char* tag, cudaEvent_t a, cudaEvent_t b, double bytes,
+                   double link_bytes) {
   std::lock_guard<std::mutex> lk(ts().mu);
-  ts().pending.push_back({tag, a, b, bytes});
+  ts().pending.push_back({tag, a, b, bytes, link_bytes});
 }
 
 std::vector<TimingRec> timing_collect() {
@@ -162,12 +164,13 @@ std::vector<TimingRec> timing_collect() {
     SFG_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
     auto it = std::find_if(out.begin(), out.end(), [&](const TimingRec& r) { return r.tag == p.tag; });
     if (it == out.end()) {
-      out.push_back(TimingRec{p.tag, 0, 0.0, 0.0});
+      out.push_back(TimingRec{p.tag, 0, 0.0, 0.0, 0.0});
       it = out.end() - 1;
     }
     it->launches++;
     it->total_ms += ms;
     it->bytes += p.bytes;
+    it->link_bytes += p.link_bytes;
     std::lock_guard<std::mutex> lk(ts().mu);
     ts().pool.push_back(p.a);
     ts().pool.push_back(p.b);

@@ -73,7 +73,7 @@ void check_unit_op(const Unit& u, ReduceOp op);
 // ------------------------------------------------------------------- config
 // /root/reference/proj/include/sf/comm.hpp:54-66
 struct CommConfig {
-  std::string backend = "threads";  // threads (in-process ranks) | nccl
+  std::string backend = "threads";  // threads (in-process ranks) | nccl | p2p
   bool deterministic = true;        // reference fold order, bit-exact
   bool debug_checksum = false;      // verify source buffers between begin/end
   bool force_remote = false;        // route self edges through the transport
@@ -105,10 +105,12 @@ struct TimingRec {
   uint64_t launches = 0;
   double total_ms = 0.0;
   double bytes = 0.0;
+  double link_bytes = 0.0;  // stored into peer GPUs (p2p puts)
 };
 void timing_enable(bool on);
 bool timing_enabled();
-void timing_record(const char* tag, cudaEvent_t a, cudaEvent_t b, double bytes);
+void timing_record(const char* tag, cudaEvent_t a, cudaEvent_t b, double bytes,
+                   double link_bytes = 0.0);
 std::vector<TimingRec> timing_collect();  // synchronises the events
 cudaEvent_t timing_event();
 
@@ -237,6 +239,8 @@ class Comm {
   Transport& transport();
   uint64_t next_op_seq() { return ++op_seq_; }
   void bind_device() const;
+  // One-sided put/signal data plane over NVLink peer mappings (backend "p2p").
+  bool p2p() const { return cfg_.backend == "p2p"; }
 
   // Every transport call of this communicator runs on one internal stream
   // (NCCL requires a single issue order per communicator); fork/join order it
@@ -309,12 +313,29 @@ struct DevPlan {
   int32_t* csr_ent = nullptr;
   int64_t csr_self_entries = 0;
   int64_t csr_remote_entries = 0;
+  // L2 tiling of the self contributions: boundaries at multiples of
+  // csr_piece_leaves leaf indices, csr_np_max - 1 per root (row-major).
+  int32_t csr_np_max = 1;
+  int64_t csr_piece_leaves = 0;
+  int32_t* csr_ptab = nullptr;
   // remote-only CSR: just the roots that receive remote contributions
   int64_t rcsr_n = 0;
   int32_t* rcsr_roots = nullptr;
   int32_t* rcsr_off = nullptr;  // [rcsr_n + 1]
   int32_t* rcsr_ent = nullptr;
   ~DevPlan();
+};
+
+// Where this rank writes inside peer r's staging slot (p2p backend). The
+// slot is one allocation [leaf_stage | root_stage | leaf_reply | flags],
+// mapped into every neighbor (CUDA IPC across processes, a plain peer pointer
+// between threads of one process).
+struct PeerSlot {
+  char* base = nullptr;   // peer's slot allocation as mapped here
+  bool ipc = false;       // opened with cudaIpcOpenMemHandle
+  size_t root_at = 0, reply_at = 0, flags_at = 0;  // byte offsets inside the slot
+  int64_t leaf_off = -1;  // peer's leaf-stage vertex offset of my group (its rg)
+  int64_t root_off = -1;  // peer's root-stage vertex offset of my group (its lg)
 };
 
 struct Staging {
@@ -325,8 +346,40 @@ struct Staging {
   unsigned long long* digest = nullptr;
   cudaEvent_t released = nullptr;
   bool released_recorded = false;
+  unsigned long long released_capture = 0;  // capture id the release was recorded in (0: none)
   bool in_use = false;
   size_t leaf_bytes = 0, root_bytes = 0;
+  // p2p: one allocation holding the three stages (regions: 0 leaf stage,
+  // 1 root stage, 2 leaf reply) and the flags
+  //   arrive[3][P], free[3][P]  (uint64, written by peers)
+  //   sent[3][P], recvd[3][P]   (uint64 local message counters)
+  //   seg_counts[kMaxPeers], done_count (uint32 CTA arrival counters)
+  // Per directed pair and region: the n-th put from me into region g of
+  // peer d waits for free[g][d] >= n-1 (d consumed my previous message
+  // there) and raises d.arrive[g][me] = n; the n-th message from s into my
+  // region g is consumed after arrive[g][s] >= n and acknowledged with
+  // s.free[g][me] = n. (One channel per region keeps fetch-and-op's reply
+  // puts independent of the acknowledgement of the request they answer.)
+  // The kernels advance the counters themselves — no host bookkeeping — so
+  // operations can be captured into a CUDA graph and replayed.
+  void* slot_mem = nullptr;
+  unsigned long long* flags = nullptr;
+  unsigned int* seg_counts = nullptr;
+  unsigned int* done_count = nullptr;
+  int nranks = 0;
+  unsigned long long* sent(int g, int r) const { return flags + (6 + g) * nranks + r; }
+  unsigned long long* recvd(int g, int r) const { return flags + (9 + g) * nranks + r; }
+  std::vector<PeerSlot> peers;  // by rank
+  const unsigned long long* arrive_flag(int g, int src) const { return flags + g * nranks + src; }
+  const unsigned long long* free_flag(int g, int dst) const { return flags + (3 + g) * nranks + dst; }
+  unsigned long long* peer_arrive_flag(int g, int peer, int me) const {
+    const PeerSlot& p = peers[static_cast<size_t>(peer)];
+    return reinterpret_cast<unsigned long long*>(p.base + p.flags_at) + g * nranks + me;
+  }
+  unsigned long long* peer_free_flag(int g, int peer, int me) const {
+    const PeerSlot& p = peers[static_cast<size_t>(peer)];
+    return reinterpret_cast<unsigned long long*>(p.base + p.flags_at) + (3 + g) * nranks + me;
+  }
   ~Staging();
 };
 
@@ -360,6 +413,7 @@ class StarForest {
   void ensure_csr();
   Staging* acquire_staging(size_t ub, cudaStream_t stream);
   void release_staging(Staging* s, cudaStream_t stream);
+  void p2p_attach(Staging& s);  // collective: allocate the slot, map it into the neighbors
 
   int32_t remote_rank_of(int64_t o) const { return remote_rank_[static_cast<size_t>(o)]; }
   int64_t remote_off_of(int64_t o) const { return remote_off_[static_cast<size_t>(o)]; }
@@ -400,6 +454,7 @@ struct OpHandle {
   Staging* stg = nullptr;
   std::vector<XferOp> recvs;        // phase-1 receives
   std::vector<XferOp> reply_recvs;  // fetch-and-op replies
+  bool forked = false;              // p2p: the puts ran on the comm stream
   std::vector<uint8_t> zero_copy_recv;
   // debug checksum
   const void* ck_ptr = nullptr;

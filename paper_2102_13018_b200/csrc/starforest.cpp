@@ -21,6 +21,14 @@ namespace sfg {
 
 namespace {
 constexpr int64_t kI32Max = (int64_t(1) << 31) - 1;
+
+// Id of the stream capture `s` takes part in, 0 when it is not capturing.
+unsigned long long capture_id(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  unsigned long long id = 0;
+  SFG_CUDA(cudaStreamGetCaptureInfo(s, &st, &id));
+  return st == cudaStreamCaptureStatusActive ? id : 0;
+}
 }
 
 DevPlan::~DevPlan() {
@@ -29,9 +37,15 @@ DevPlan::~DevPlan() {
 }
 
 Staging::~Staging() {
-  if (leaf_stage) cudaFree(leaf_stage);
-  if (root_stage) cudaFree(root_stage);
-  if (leaf_reply) cudaFree(leaf_reply);
+  for (auto& p : peers)
+    if (p.ipc && p.base) cudaIpcCloseMemHandle(p.base);
+  if (slot_mem) {
+    cudaFree(slot_mem);
+  } else {
+    if (leaf_stage) cudaFree(leaf_stage);
+    if (root_stage) cudaFree(root_stage);
+    if (leaf_reply) cudaFree(leaf_reply);
+  }
   if (digest) cudaFree(digest);
   if (released) cudaEventDestroy(released);
 }
@@ -417,6 +431,28 @@ void StarForest::ensure_csr() {
   d.csr_self_entries = self ? static_cast<int64_t>(leaf_groups_.front().items.size()) : 0;
   d.csr_remote_entries = total - d.csr_self_entries;
 
+  // L2 tiling (kernels.cu run_csr_warp): where the leaf array the self
+  // contributions gather from is several times larger than L2, record per
+  // root the first self entry at or beyond each multiple of kPiece leaves.
+  constexpr int64_t kPiece = int64_t(1) << 21;
+  std::vector<int32_t> ptab;
+  const int64_t np_max = (leaf_bound_ + kPiece - 1) / kPiece;
+  const int64_t mean_deg = roots.empty() ? 0 : total / static_cast<int64_t>(roots.size());
+  if (np_max >= 3 && mean_deg >= 8 && d.csr_self_entries > 0) {
+    const int64_t cols = np_max - 1;
+    ptab.resize(roots.size() * static_cast<size_t>(cols));
+    for (size_t q = 0; q < roots.size(); ++q) {
+      int64_t j = offs[q];
+      const int64_t end = split[q];
+      for (int64_t b = 1; b <= cols; ++b) {
+        while (j < end && ent[static_cast<size_t>(j)] < b * kPiece) ++j;
+        ptab[q * static_cast<size_t>(cols) + static_cast<size_t>(b - 1)] = static_cast<int32_t>(j);
+      }
+    }
+    d.csr_np_max = static_cast<int32_t>(np_max);
+    d.csr_piece_leaves = kPiece;
+  }
+
   // Remote-only view: the (usually few) roots with remote contributions, so
   // the End-side fold does not walk every root of the forest.
   std::vector<int32_t> rroots, roffs, rent;
@@ -431,7 +467,7 @@ void StarForest::ensure_csr() {
   d.rcsr_n = static_cast<int64_t>(rroots.size());
 
   const size_t bytes = (roots.size() + offs.size() + split.size() + ent.size() + rroots.size() +
-                        roffs.size() + rent.size()) * sizeof(int32_t);
+                        roffs.size() + rent.size() + ptab.size()) * sizeof(int32_t);
   if (bytes) {
     SFG_CUDA(cudaMalloc(&d.csr_blob, bytes));
     auto* p = static_cast<int32_t*>(d.csr_blob);
@@ -447,6 +483,8 @@ void StarForest::ensure_csr() {
     put(rroots, d.rcsr_roots);
     put(roffs, d.rcsr_off);
     put(rent, d.rcsr_ent);
+    put(ptab, d.csr_ptab);
+    if (ptab.empty()) d.csr_ptab = nullptr;
   }
   d.csr_built = true;
 }
@@ -456,15 +494,22 @@ Staging* StarForest::acquire_staging(size_t ub, cudaStream_t stream) {
   for (auto& s : staging_) {
     if (s->in_use || s->unit_bytes != ub) continue;
     s->in_use = true;
-    if (s->released_recorded) SFG_CUDA(cudaStreamWaitEvent(stream, s->released, 0));
+    if (s->released_recorded && s->released_capture == capture_id(stream))
+      SFG_CUDA(cudaStreamWaitEvent(stream, s->released, 0));
+    // else: released outside the CUDA graph being captured now; capture
+    // starts after that work completed (cudaStreamBeginCapture contract).
     return s.get();
   }
   auto s = std::make_unique<Staging>();
   s->unit_bytes = ub;
   s->leaf_bytes = static_cast<size_t>(d.n_leafside) * ub;
   s->root_bytes = static_cast<size_t>(d.n_rootside) * ub;
-  if (s->leaf_bytes) SFG_CUDA(cudaMalloc(&s->leaf_stage, s->leaf_bytes));
-  if (s->root_bytes) SFG_CUDA(cudaMalloc(&s->root_stage, s->root_bytes));
+  if (comm_->p2p()) {
+    p2p_attach(*s);
+  } else {
+    if (s->leaf_bytes) SFG_CUDA(cudaMalloc(&s->leaf_stage, s->leaf_bytes));
+    if (s->root_bytes) SFG_CUDA(cudaMalloc(&s->root_stage, s->root_bytes));
+  }
   SFG_CUDA(cudaMalloc(&s->digest, sizeof(unsigned long long)));
   SFG_CUDA(cudaEventCreateWithFlags(&s->released, cudaEventDisableTiming));
   s->in_use = true;
@@ -475,6 +520,7 @@ Staging* StarForest::acquire_staging(size_t ub, cudaStream_t stream) {
 void StarForest::release_staging(Staging* s, cudaStream_t stream) {
   SFG_CUDA(cudaEventRecord(s->released, stream));
   s->released_recorded = true;
+  s->released_capture = capture_id(stream);
   s->in_use = false;
 }
 

@@ -131,7 +131,7 @@ def _lib():
 @dataclass
 class CommConfig:  # comm.hpp:54-66
     nranks: int = 1
-    backend: str = "threads"  # threads | nccl
+    backend: str = "threads"  # threads | nccl | p2p
     deterministic: bool = True
     debug_checksum: bool = False
     force_remote: bool = False
@@ -641,13 +641,14 @@ def timing_enable(on: bool = True) -> None:
 
 
 def timing_collect() -> dict:
-    """{tag: {"launches", "total_ms", "bytes"}} for launches since the last collect."""
+    """{tag: {"launches", "total_ms", "bytes", "link_bytes"}} for launches since the last collect."""
     cap = 64
     arr = (L.sfg_timing * cap)()
     n = C.c_int()
     _check(_lib().sfg_timing_collect(arr, cap, C.byref(n)))
     return {arr[i].tag.decode(): {"launches": arr[i].launches, "total_ms": arr[i].total_ms,
-                                  "bytes": arr[i].bytes} for i in range(n.value)}
+                                  "bytes": arr[i].bytes, "link_bytes": arr[i].link_bytes}
+            for i in range(n.value)}
 
 
 # ----------------------------------------------------------------- harness

@@ -23,10 +23,11 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     fails = []
+    backend = sys.argv[1] if len(sys.argv) > 1 else "nccl"
     for deterministic in (True, False):
         obj = [sf.nccl_unique_id() if rank == 0 else None]  # one id per communicator
         dist.broadcast_object_list(obj, src=0)
-        comm = sf.Comm(world, rank, local, sf.CommConfig(nranks=world, backend="nccl",
+        comm = sf.Comm(world, rank, local, sf.CommConfig(nranks=world, backend=backend,
                                                          deterministic=deterministic), nccl_id=obj[0])
         cases = [("g2l", [graphs.g2l_halo(9, world, r) for r in range(world)])]
         for seed in range(4):
@@ -71,6 +72,40 @@ def main():
                     assert_same([a[4] for a in allr], O.gather(specs, leaves), what=f"{name} gather")
                 except AssertionError as e:
                     fails.append(f"det={deterministic} {e}")
+            if name.startswith("rand") and deterministic:
+                # CUDA-graph capture of Bcast(REPLACE) + Reduce(SUM): replayed with new
+                # root values it must give what eager calls give (the p2p protocol's
+                # message counters live on the device).
+                st = torch.cuda.Stream()
+                r0 = dev(roots[rank])
+                lg = dev(leaves[rank])
+                racc = dev(roots[rank])
+                with torch.cuda.stream(st):
+                    for _ in range(2):
+                        sf.bcast_end(sf.bcast_begin(f, u, r0, lg, sf.ReduceOp.replace, st))
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st):
+                    sf.bcast_end(sf.bcast_begin(f, u, r0, lg, sf.ReduceOp.replace, st))
+                    sf.reduce_end(sf.reduce_begin(f, u, lg, racc, sf.ReduceOp.sum, st))
+                for it in range(3):
+                    r0.copy_(dev(roots[rank] * (it + 2)))
+                    racc.copy_(dev(roots[rank]))
+                    g.replay()
+                    torch.cuda.synchronize()
+                    got = [lg.cpu().numpy(), racc.cpu().numpy()]
+                    allg = [None] * world
+                    dist.all_gather_object(allg, got)
+                    if rank == 0:
+                        try:
+                            scaled = [x * (it + 2) for x in roots]
+                            wl = O.bcast(specs, scaled, leaves)
+                            assert_same([a[0] for a in allg], wl, what=f"{name} graph bcast {it}")
+                            assert_same([a[1] for a in allg], O.reduce(specs, wl, roots, "sum"),
+                                        what=f"{name} graph reduce {it}")
+                        except AssertionError as e:
+                            fails.append(f"graph {e}")
+                del g
             del f
         comm.close()
     dist.barrier()
@@ -79,7 +114,7 @@ def main():
         if fails:
             print("FAIL", *fails, sep="\n")
             sys.exit(1)
-        print(f"mp_worker ok world={world}")
+        print(f"mp_worker ok world={world} backend={backend}")
 
 
 if __name__ == "__main__":

@@ -26,7 +26,7 @@ need2 = pytest.mark.skipif("ngpu() < 2")
 
 
 @need2
-@pytest.mark.parametrize("backend", ["nccl", "threads"])
+@pytest.mark.parametrize("backend", ["nccl", "threads", "p2p"])
 def test_threads_of_one_process_on_distinct_gpus(backend):
     n = min(ngpu(), 4)
     devices = list(range(n))
@@ -49,27 +49,97 @@ def test_threads_of_one_process_on_distinct_gpus(backend):
 
 
 @need2
-def test_g2l_halo_over_nccl():
+@pytest.mark.parametrize("backend", ["nccl", "p2p"])
+def test_g2l_halo(backend):
     n = min(ngpu(), 4)
     specs = [graphs.g2l_halo(24, n, r) for r in range(n)]
     geo = [graphs.G2L(24, n, r) for r in range(n)]
     roots = [graphs.gen_f64(2, r, g.n_owned) for r, g in enumerate(geo)]
     leaves = [np.zeros(g.n_local) for g in geo]
-    out = run_gpu(specs, "bcast", [roots, leaves], config=sf.CommConfig(backend="nccl"),
+    out = run_gpu(specs, "bcast", [roots, leaves], config=sf.CommConfig(backend=backend),
                   devices=list(range(n)))
     want = O.bcast(specs, roots, leaves)
     assert_same(out[1], want)
-    out = run_gpu(specs, "reduce", [want, roots], op="sum", config=sf.CommConfig(backend="nccl"),
+    out = run_gpu(specs, "reduce", [want, roots], op="sum", config=sf.CommConfig(backend=backend),
                   devices=list(range(n)))
     assert_same(out[1], O.reduce(specs, want, roots, "sum"))
 
 
 @need2
-def test_process_per_gpu_torchrun():
+def test_p2p_outstanding_handles_and_slot_reuse():
+    """ops.hpp:28-30 / test_sfops.cpp:219-237 over the one-sided backend:
+    several handles in flight on one forest (distinct staging slots), Ends
+    out of Begin order, mixed unit sizes, many epochs per slot."""
+    import torch
+
     n = min(ngpu(), 4)
+    specs = graphs.random_graph_specs(5, n, 300)
+    roots = rank_data(specs, 1, np.float64, 1, 100, "root")
+    leaves = rank_data(specs, 1, np.float64, 1, 200, "leaf")
+    iroots = rank_data(specs, 1, np.int64, 3, 300, "root", 1, 1000)
+    ileaves = rank_data(specs, 1, np.int64, 3, 400, "leaf", 1, 1000)
+    want_b = O.bcast(specs, roots, leaves)
+    want_r = O.reduce(specs, ileaves, iroots, "sum", 3)
+    u = sf.Unit(sf.Kind.float64)
+    ui = sf.Unit(sf.Kind.int64, 3)
+
+    def body(comm):
+        r = comm.rank()
+        f = sf.StarForest(comm)
+        f.set_graph_spec(specs[r])
+        f.setup()
+        st = torch.cuda.Stream()
+        out = []
+        with torch.cuda.stream(st):
+            for it in range(6):
+                root = torch.from_numpy(roots[r]).cuda()
+                leaf = torch.from_numpy(leaves[r]).cuda()
+                iroot = torch.from_numpy(iroots[r]).cuda()
+                ileaf = torch.from_numpy(ileaves[r]).cuda()
+                h1 = sf.bcast_begin(f, u, root, leaf, sf.ReduceOp.replace, st)
+                h2 = sf.reduce_begin(f, ui, ileaf, iroot, sf.ReduceOp.sum, st)
+                if it % 2:
+                    sf.bcast_end(h1)
+                    sf.reduce_end(h2)
+                else:
+                    sf.reduce_end(h2)
+                    sf.bcast_end(h1)
+                out.append((leaf.cpu().numpy(), iroot.cpu().numpy()))
+        st.synchronize()
+        return out
+
+    got = sf.run_ranks(sf.CommConfig(nranks=n, backend="p2p"), body, devices=list(range(n)))
+    for it in range(6):
+        assert_same([g[it][0] for g in got], want_b, what=f"iter {it} bcast")
+        assert_same([g[it][1] for g in got], want_r, what=f"iter {it} reduce")
+
+
+@need2
+def test_p2p_needs_one_gpu_per_rank():
+    import torch
+
+    specs = graphs.random_graph_specs(3, 2, 20)
+
+    def body(comm):
+        f = sf.StarForest(comm)
+        f.set_graph_spec(specs[comm.rank()])
+        f.setup()
+        root = torch.zeros(int(specs[comm.rank()].nroots), dtype=torch.float64, device="cuda")
+        leaf = torch.zeros(specs[comm.rank()].leaf_bound(), dtype=torch.float64, device="cuda")
+        sf.bcast(f, sf.Unit(sf.Kind.float64), root, leaf, sf.ReduceOp.replace)
+
+    with pytest.raises(sf.HarnessError, match="one GPU per rank"):
+        sf.run_ranks(sf.CommConfig(nranks=2, backend="p2p"), body, devices=[0, 0])
+
+
+@need2
+@pytest.mark.parametrize("backend", ["nccl", "p2p"])
+def test_process_per_gpu_torchrun(backend):
+    n = min(ngpu(), 4)
+    port = "29533" if backend == "nccl" else "29534"
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port",
-                        "29533", os.path.join(ROOT, "tests", "mp_worker.py")],
+                        port, os.path.join(ROOT, "tests", "mp_worker.py"), backend],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "mp_worker ok" in r.stdout

@@ -159,6 +159,31 @@ def test_split_transparency_force_remote(seed):
     assert_same(b[2], a[2])
 
 
+@pytest.mark.parametrize("seed", SEEDS[:4])
+def test_p2p_put_path_single_rank_force_remote(seed):
+    """The one-sided put/signal path (backend p2p) on one GPU: with
+    force_remote the self edges become a remote group whose put kernel stores
+    into this rank's own mapped slot, raises its arrive flag and frees it —
+    the same kernels and stream waits the multi-GPU path runs."""
+    specs = graphs.random_graph_specs(seed * 31 + 7, 1, 400)
+    roots = rank_data(specs, seed, np.float64, 2, 100, "root")
+    leaves = rank_data(specs, seed, np.float64, 2, 200, "leaf")
+    cfg = lambda: sf.CommConfig(backend="p2p", force_remote=True)  # noqa: E731
+    out = run_gpu(specs, "bcast", [roots, leaves], op="replace", blocklen=2, config=cfg())
+    assert_same(out[1], O.bcast(specs, roots, leaves, "replace", 2), what="bcast")
+    out = run_gpu(specs, "reduce", [leaves, roots], op="sum", blocklen=2, config=cfg())
+    assert_same(out[1], O.reduce(specs, leaves, roots, "sum", 2), what="reduce")
+    upd = [np.zeros_like(x) for x in leaves]
+    r, _, u = run_gpu(specs, "fetch_and_op", [roots, leaves, upd], op="sum", blocklen=2, config=cfg())
+    orr, ou = O.fetch_and_op(specs, roots, leaves, upd, "sum", 2)
+    assert_same(r, orr, what="fetch root")
+    assert_same(u, ou, what="fetch update")
+    deg = O.degrees(specs)
+    multi = [np.zeros(int(d.sum()) * 2) for d in deg]
+    out = run_gpu(specs, "gather", [leaves, multi], blocklen=2, config=cfg())
+    assert_same(out[1], O.gather(specs, leaves, 2), what="gather")
+
+
 @pytest.mark.parametrize("seed", SEEDS[:6])
 def test_free_order_mode(seed):
     """deterministic=False: integer results exact, float within 1e-12, fetch
@@ -311,6 +336,23 @@ def test_config4_high_contention(P, dtype):
     out = run_gpu(specs, "reduce", [leaves, roots], op="sum")
     assert_same(out[1], O.reduce(specs, leaves, roots, "sum"))
     upd = [np.zeros_like(l) for l in leaves]
+    r, _, u = run_gpu(specs, "fetch_and_op", [roots, leaves, upd], op="sum")
+    orr, ou = O.fetch_and_op(specs, roots, leaves, upd, "sum")
+    assert_same(r, orr)
+    assert_same(u, ou)
+
+
+def test_csr_l2_pieces_exact_order():
+    """Leaf array (64 MB) several times a 16 MB piece: the warp CSR walks
+    L2-sized leaf windows piece-major (kernels.cu run_csr_warp). Fold order
+    per root is unchanged, so float64 Reduce/FetchAndOp stay bit-exact."""
+    L, R = 1 << 23, 1 << 16
+    specs = graphs.random_leaf_root(L, R, 1, seed=4)
+    roots = rank_data(specs, 4, np.float64, 1, 100, "root", 1, 1000)
+    leaves = rank_data(specs, 4, np.float64, 1, 200, "leaf", 1, 1000)
+    out = run_gpu(specs, "reduce", [leaves, roots], op="sum")
+    assert_same(out[1], O.reduce(specs, leaves, roots, "sum"))
+    upd = [np.zeros_like(x) for x in leaves]
     r, _, u = run_gpu(specs, "fetch_and_op", [roots, leaves, upd], op="sum")
     orr, ou = O.fetch_and_op(specs, roots, leaves, upd, "sum")
     assert_same(r, orr)
