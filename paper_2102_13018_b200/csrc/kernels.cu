@@ -544,16 +544,28 @@ __device__ __forceinline__ void wait_flags(const LaunchParams& P, uint32_t mask)
   __syncthreads();
 }
 
+// CTA arrival counter with acquire-release semantics at GPU scope: orders
+// this CTA's prior loads and stores (peer stores over NVLink included) before
+// the increment, and everything the last CTA observed before its own
+// system-scope release. The PTX memory model makes causality transitive
+// across scopes (CTA barrier -> GPU-scope atomic -> system-scope release ->
+// the peer's system-scope acquire), so one MEMBAR.SYS by the last CTA
+// replaces a fence.sc.sys per CTA — measured on B200 (scripts/p2p_microbench.cu,
+// profiles/r1_p2p_microbench.md): 2 MB put + flag 13.0 us -> 6.5 us, 8 B
+// put + flag 5.1 us -> 3.7 us.
+__device__ __forceinline__ unsigned int cta_arrive(unsigned int* counter) {
+  unsigned int prev;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(counter) : "memory");
+  return prev;
+}
+
 // Launch completion: the last CTA raises every done flag (after all CTAs'
-// reads of the slot and stores are fenced).
+// reads of the slot and stores).
 __device__ __forceinline__ void signal_launch_done(const LaunchParams& P) {
   __syncthreads();
   if (threadIdx.x != 0) return;
-  __threadfence_system();
-  const unsigned int prev = atomicAdd(P.done_count, 1u);
-  if (prev + 1 == gridDim.x) {
+  if (cta_arrive(P.done_count) + 1 == gridDim.x) {
     *P.done_count = 0u;
-    __threadfence_system();
     for (int i = 0; i < P.ndone; ++i) {
       const unsigned long long v = *P.done_seq[i] + 1;
       *P.done_seq[i] = v;
@@ -562,18 +574,15 @@ __device__ __forceinline__ void signal_launch_done(const LaunchParams& P) {
   }
 }
 
-// Put completion: every CTA of the segment fences its stores (peer stores
-// over NVLink included) at system scope and counts itself in; the last one
-// publishes the segment's flag with a system-scope release store, which the
-// receiving GPU's stream waits on (cuStreamWaitValue64, ops.cpp).
+// Put completion: every CTA of the segment counts itself in after its stores
+// (into the peer's slot over NVLink); the last one publishes the segment's
+// flag with a system-scope release store, which the receiving GPU's unpack
+// kernel acquires (wait_flags).
 __device__ __forceinline__ void signal_segment_done(const DSeg& seg, int64_t nblk) {
   __syncthreads();
   if (threadIdx.x != 0) return;
-  __threadfence_system();
-  const unsigned int prev = atomicAdd(seg.sig_count, 1u);
-  if (static_cast<int64_t>(prev) + 1 == nblk) {
+  if (static_cast<int64_t>(cta_arrive(seg.sig_count)) + 1 == nblk) {
     *seg.sig_count = 0u;  // ready for the next launch on this stream
-    __threadfence_system();
     const unsigned long long v = *seg.sig_seq + 1;
     *seg.sig_seq = v;
     st_release_sys(seg.sig_flag, v);
@@ -584,7 +593,7 @@ __device__ __forceinline__ void signal_segment_done(const DSeg& seg, int64_t nbl
 // launches (every pack, unpack and structured local scatter) get their own
 // instantiation so the CSR paths do not raise their register allocation.
 template <class T, int OP, bool FULL>
-__global__ void __launch_bounds__(kThreads) segments_kernel(const __grid_constant__ LaunchParams P) {
+__global__ void __launch_bounds__(kThreads, FULL ? 3 : 4) segments_kernel(const __grid_constant__ LaunchParams P) {
   const int64_t b = blockIdx.x;
   int s = 0;
   while (s + 1 < P.nseg && b >= P.block_start[s + 1]) ++s;

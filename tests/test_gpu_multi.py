@@ -115,6 +115,48 @@ def test_p2p_outstanding_handles_and_slot_reuse():
 
 
 @need2
+def test_p2p_stress_visibility():
+    """Every put is followed by a single system-scope release from the last
+    CTA (kernels.cu cta_arrive): 300 back-to-back Bcast+Reduce rounds on a
+    halo SF with 120K ghost points per face, values changing every round,
+    checked on the device after every round — any ghost read before its
+    data landed shows up as a mismatch."""
+    import torch
+
+    n = 2
+    N = 96
+    specs = [graphs.g2l_halo(N, n, r) for r in range(n)]
+    geo = [graphs.G2L(N, n, r) for r in range(n)]
+    roots = [graphs.gen_f64(3, r, g.n_owned) for r, g in enumerate(geo)]
+    zeros = [np.zeros(g.n_local) for g in geo]
+    want_leaf = O.bcast(specs, roots, zeros)
+    u = sf.Unit(sf.Kind.float64)
+
+    def body(comm):
+        r = comm.rank()
+        f = sf.StarForest(comm)
+        f.set_graph_spec(specs[r])
+        f.setup()
+        st = torch.cuda.Stream()
+        base = torch.from_numpy(roots[r]).cuda()
+        wl = torch.from_numpy(want_leaf[r]).cuda()
+        root = torch.empty_like(base)
+        leaf = torch.zeros(geo[r].n_local, dtype=torch.float64, device="cuda")
+        bad = torch.zeros((), dtype=torch.int64, device="cuda")
+        with torch.cuda.stream(st):
+            for it in range(1, 301):
+                root.copy_(base * it)
+                sf.bcast_end(sf.bcast_begin(f, u, root, leaf, sf.ReduceOp.replace, st))
+                bad += (leaf != wl * it).sum()
+                sf.reduce_end(sf.reduce_begin(f, u, leaf, root, sf.ReduceOp.replace, st))
+        st.synchronize()
+        return int(bad.item())
+
+    got = sf.run_ranks(sf.CommConfig(nranks=n, backend="p2p"), body, devices=[0, 1])
+    assert got == [0, 0]
+
+
+@need2
 def test_p2p_needs_one_gpu_per_rank():
     import torch
 
