@@ -96,16 +96,20 @@ class Ctx:
         torch.cuda.synchronize()
         self.barrier()
         sf.timing_collect()
-        # Flush L2 (write 256 MB) before every timed call: the config-1/4
-        # working sets fit in the 126 MB L2 and would otherwise be timed hot.
-        flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        # Flush L2 before every timed call: the config-1/4 working sets fit in
+        # the 126 MB L2 and would otherwise be timed hot. The flush READS a
+        # 256 MB buffer (L2 left full of clean lines): a write-based flush
+        # leaves ~126 MB of dirty lines whose write-back would be charged to
+        # the timed kernel.
+        flush_buf = torch.ones(64 << 20, dtype=torch.int32, device="cuda")
+        flush_out = torch.empty((), dtype=torch.int64, device="cuda")
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(steps)]
         sf.timing_enable(True)
         with torch.cuda.stream(self.stream):
             for e0, e1 in evs:
                 if flush:
-                    flush_buf.zero_()
+                    torch.sum(flush_buf, dim=0, dtype=torch.int64, out=flush_out)
                 e0.record(self.stream)
                 fn()
                 e1.record(self.stream)

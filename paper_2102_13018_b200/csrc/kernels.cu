@@ -274,12 +274,11 @@ __device__ __forceinline__ void run_pair_rows(const DSeg& s, const LaunchParams&
 // groups ascending rank, each in ascending leaf order). Sequential per root,
 // so floating-point results are bit-identical to the CPU reference.
 // Sequential fold of contributions [lo, hi) of one root item by one thread,
-// 8 contributions in flight (entries, then values, then the dependent fold).
-template <class T, int OP>
+// kB contributions in flight (entries, then values, then the dependent fold).
+template <class T, int OP, int kB = 8>
 __device__ __forceinline__ T csr_thread_range(const DSeg& s, const T* leaf, T* stage, T* aux,
                                               int64_t bl, int64_t k, int32_t lo, int32_t hi, T acc,
                                               bool fetch) {
-  constexpr int kB = 8;
   for (int32_t j = lo; j < hi; j += kB) {
     int32_t en[kB];
     T c[kB];
@@ -318,7 +317,7 @@ __device__ __forceinline__ void csr_piece(const DSeg& s, int64_t r, int q, int32
 // the CPU reference, and a warp instruction advances 32 roots at once.
 // With pieces (csr_np > 1) the grid walks L2-sized leaf windows piece-major
 // (see run_csr_warp).
-template <class T, int OP>
+template <class T, int OP, int kB = 8>
 __device__ __forceinline__ void run_csr(const DSeg& s, const LaunchParams& P, int64_t blk,
                                         bool fetch) {
   T* root = static_cast<T*>(P.bufs[s.dst_buf]);
@@ -337,7 +336,7 @@ __device__ __forceinline__ void run_csr(const DSeg& s, const LaunchParams& P, in
     const int32_t hi = __ldg(s.csr_hi + r);
     if (lo >= hi) return;
     const int64_t ro = static_cast<int64_t>(__ldg(s.csr_roots + r)) * bl + k;
-    root[ro] = csr_thread_range<T, OP>(s, leaf, stage, aux, bl, k, lo, hi, root[ro], fetch);
+    root[ro] = csr_thread_range<T, OP, kB>(s, leaf, stage, aux, bl, k, lo, hi, root[ro], fetch);
     return;
   }
   for (int q = 0; q < s.csr_np; ++q) {
@@ -348,7 +347,7 @@ __device__ __forceinline__ void run_csr(const DSeg& s, const LaunchParams& P, in
       csr_piece(s, r, q, lo, hi);
       if (lo >= hi) continue;
       const int64_t ro = static_cast<int64_t>(__ldg(s.csr_roots + r)) * bl + k;
-      root[ro] = csr_thread_range<T, OP>(s, leaf, stage, aux, bl, k, lo, hi, root[ro], fetch);
+      root[ro] = csr_thread_range<T, OP, kB>(s, leaf, stage, aux, bl, k, lo, hi, root[ro], fetch);
     }
   }
 }
@@ -648,6 +647,18 @@ __global__ void __launch_bounds__(kThreads, FULL ? 3 : 4) segments_kernel(const 
   if (P.ndone > 0) signal_launch_done(P);
 }
 
+// A launch that is one thread-per-root CSR segment runs in its own kernel:
+// kB = 8 at ≤ 64 registers (4 CTAs/SM) for low-degree roots, where many
+// roots in flight hide the latency; kB = 32 (2 CTAs/SM) for high-degree
+// roots, where each thread must keep many contributions in flight itself.
+template <class T, int OP, int kB>
+__global__ void __launch_bounds__(kThreads, kB >= 32 ? 2 : 4) csr_kernel(const __grid_constant__ LaunchParams P) {
+  const DSeg& seg = P.seg[0];
+  if (seg.wait_mask) wait_flags(P, seg.wait_mask);
+  if constexpr (OP != OP_REPLACE) run_csr<T, OP, kB>(seg, P, blockIdx.x, seg.type == SEG_CSR_FETCH);
+  if (P.ndone > 0) signal_launch_done(P);
+}
+
 template <class T, int OP>
 void launch_t(const LaunchParams& p, int64_t blocks, cudaStream_t st) {
   bool full = false;
@@ -655,6 +666,10 @@ void launch_t(const LaunchParams& p, int64_t blocks, cudaStream_t st) {
     full = full || (p.seg[s].type != SEG_PAIR && p.seg[s].type != SEG_PAIR_ATOMIC);
   if constexpr (OP == OP_REPLACE) {
     segments_kernel<T, OP, false><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
+  } else if (p.nseg == 1 && (p.seg[0].type == SEG_CSR_FOLD || p.seg[0].type == SEG_CSR_FETCH) &&
+             !p.seg[0].csr_warp && (std::is_same_v<T, double> || std::is_same_v<T, int64_t> ||
+                                    std::is_same_v<T, int32_t>)) {
+    csr_kernel<T, OP, 8><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
   } else {
     if (full)
       segments_kernel<T, OP, true><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
@@ -711,8 +726,11 @@ __global__ void digest_kernel(const unsigned char* p, size_t bytes, unsigned lon
 template <class T, int OP>
 int64_t resident_full() {
   static const int64_t v = [] {
-    int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, segments_kernel<T, OP, true>, kThreads, 0);
+    int dev = 0, sms = 0, a = 0, b = 0;
+    // the smaller residency of the two kernels a CSR segment may run in
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, segments_kernel<T, OP, true>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, csr_kernel<T, OP, 8>, kThreads, 0);
+    const int per_sm = std::min(a, b);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     return static_cast<int64_t>(std::max(1, per_sm) * std::max(1, sms));
@@ -762,11 +780,12 @@ int launch_segments(LaunchParams& p, ElemType t, int op, cudaStream_t stream) {
     p.seg[n] = p.seg[s];
     p.block_start[n] = blocks;
     const bool csr = p.seg[s].type == SEG_CSR_FOLD || p.seg[s].type == SEG_CSR_FETCH;
-    const int64_t per_block = !csr ? kThreads * kItems : p.seg[s].csr_warp ? kThreads / 32 : kThreads;
+    const int64_t per_block = !csr ? kThreads * kItems : p.seg[n].csr_warp ? kThreads / 32 : kThreads;
     int64_t nb = (items + per_block - 1) / per_block;
-    if (csr && p.seg[s].csr_np > 1) {
+    if (csr && p.seg[n].csr_np > 1) {
       // Piece-major walk: every CTA of the segment must be resident at once.
-      nb = std::min<int64_t>(nb, resident_ctas(t, op));
+      const int64_t res = resident_ctas(t, op);
+      nb = std::min<int64_t>(nb, res);
       p.seg[n].csr_grid_threads = nb * kThreads;
     }
     blocks += nb;
