@@ -371,6 +371,59 @@ def config5(ctx, args):
                "transport": ctx.transport, "rows": rows})
 
 
+# ------------------------------------------------------- config 3 consumer
+def config3_spmv(ctx, args):
+    """The ghost exchange inside its caller: y = A x with the
+    27-point Laplacian on an N^3 grid, one block of rows per GPU
+    (proc_grid(world)), spmv.hpp:149-157 on the device — the ghost Bcast is
+    overlapped with the diagonal-block product. Reported beside the same
+    product run without overlap (Bcast completed before the diagonal
+    product) and the diagonal product alone."""
+    from paper_2102_13018_b200 import graphs
+    from paper_2102_13018_b200 import spmv as S
+
+    torch, sf = ctx.torch, ctx.sf
+    N = args.n3_spmv
+    dims = graphs.proc_grid(ctx.world)
+    t0 = time.perf_counter()
+    (rp, ci, vals), layout = S.laplacian27_block(N, dims, ctx.rank)
+    m = S.split_rows(rp, ci, vals, layout, ctx.rank)
+    gen_s = time.perf_counter() - t0
+    comm = ctx.comm(True)
+    f = S.build_ghost_sf(comm, m)
+    D, B = S.Matrix(comm, m.diag), S.Matrix(comm, m.offdiag)
+    n = layout.local_size(ctx.rank)
+    x = torch.cos(torch.arange(n, dtype=torch.float64, device="cuda") * 0.37)
+    lvec = torch.zeros(len(m.garray), dtype=torch.float64, device="cuda")
+    y = torch.zeros(n, dtype=torch.float64, device="cuda")
+    u = sf.Unit(sf.Kind.float64)
+
+    def overlapped():
+        S.spmv(f, D, B, x, lvec, y, ctx.stream)
+
+    def serial():  # exchange first, then both products (no overlap)
+        h = sf.bcast_begin(f, u, x, lvec, sf.ReduceOp.replace, ctx.stream)
+        sf.bcast_end(h)
+        S.spmv(f, D, B, x, lvec, y, ctx.stream)
+
+    nnz = ctx.vsum(float(m.diag.rowptr[-1] + m.offdiag.rowptr[-1]))
+    res = {}
+    for name, fn in (("spmv_overlapped", overlapped), ("exchange_then_spmv", serial)):
+        ms, byts, rec = ctx.timed(fn, args.steps, args.warmup, flush=False)
+        res[name] = (ms, byts, rec)
+    ms_o, byts, rec = res["spmv_overlapped"]
+    ms_s = res["exchange_then_spmv"][0]
+    kern = {k: 1e3 * v["total_ms"] / v["launches"] for k, v in rec.items()}
+    emit(ctx, {"config": 3, "op": "spmv_27pt", "n_gpus": ctx.world, "grid": [N] * 3,
+               "dims": list(dims), "rows": layout.total(), "nnz": nnz,
+               "us_per_spmv": ms_o * 1e3, "us_exchange_then_spmv": ms_s * 1e3,
+               "GFLOPs": 2 * nnz / (ms_o * 1e-3) / 1e9,
+               "GBps_algorithmic": byts / (ms_o * 1e-3) / 1e9,
+               "frac_hbm_per_gpu": byts / ctx.world / (ms_o * 1e-3) / 1e9 / peak(),
+               "kernels_us_rank0": kern, "transport": ctx.transport, "gen_s": gen_s,
+               "ghosts_rank0": len(m.garray)})
+
+
 # ------------------------------------------------------------------ config 3
 def config3(ctx, args):
     """8 ranks. With 8 GPUs: one process per GPU (NCCL). Otherwise: 8 thread
@@ -453,10 +506,15 @@ def main():
     p.add_argument("--max-bytes", type=int, default=256 << 20)
     p.add_argument("--n3", type=int, default=400)
     p.add_argument("--n2", type=int, default=512)
+    p.add_argument("--n3-spmv", type=int, default=160)
+    p.add_argument("--spmv", action="store_true", help="config 3: the SpMV consumer")
     p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"])
     args = p.parse_args()
     ctx = Ctx(transport=args.transport)
-    {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}[args.config](ctx, args)
+    if args.config == 3 and args.spmv:
+        config3_spmv(ctx, args)
+    else:
+        {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}[args.config](ctx, args)
     if ctx.dist:
         ctx.dist.barrier()
         ctx.dist.destroy_process_group()

@@ -165,6 +165,26 @@ int sfg_gather_end(sfg_handle h);
 int sfg_scatter_begin(sfg_sf sf, int kind, int64_t blocklen, const void* multirootdata,
                       void* leafdata, void* stream, sfg_handle* out);
 int sfg_scatter_end(sfg_handle h);
+/* Distributed SpMV over a ghost forest — the path's consumer
+ * (spmv.hpp:147-169). A matrix block is uploaded once from host CSR arrays
+ * (Csr<T>, spmv.hpp:31-78; kind SFG_FLOAT64 or SFG_INT64) to the
+ * communicator's GPU. With ghost_sf = build_column_sf over the off-diagonal
+ * block's garray (spmv.cpp:29-43; leaves = lvec, roots = owned x):
+ *   sfg_spmv:            y = A x_owned + B lvec, the ghost Bcast overlapped
+ *                        with the diagonal product (spmv.hpp:149-157);
+ *   sfg_spmv_transpose:  y = A^T x_owned + Reduce_SUM(B^T x_owned)
+ *                        (spmv.hpp:161-169).
+ * Device pointers, stream-ordered like the operations; results are
+ * bit-identical to the reference's Csr loops (no FMA contraction). */
+typedef struct sfg_mat_s* sfg_mat;
+int sfg_mat_create(sfg_comm c, int64_t rows, int64_t cols, const int64_t* rowptr,
+                   const int64_t* colind, const void* vals, int kind, sfg_mat* out);
+int sfg_mat_destroy(sfg_mat m);
+int sfg_spmv(sfg_sf ghost_sf, sfg_mat diag, sfg_mat offdiag, const void* x_owned, void* lvec,
+             void* y, void* stream);
+int sfg_spmv_transpose(sfg_sf ghost_sf, sfg_mat diag, sfg_mat offdiag, const void* x_owned,
+                       void* lvec, void* y, void* stream);
+
 /* Handle introspection (OpHandle::kind/op/ended, ops.hpp:38-45) and release. */
 int sfg_handle_info(sfg_handle h, int* opkind, int* op, int* ended);
 int sfg_handle_free(sfg_handle h);

@@ -140,3 +140,46 @@ def scatter(specs, multiroot, leafdata, blocklen=1):
                            KIND[np.dtype(leaves[0].dtype)], blocklen, _ptrs(multi),
                            _ptrs(leaves))
     return leaves
+
+
+# ------------------------------------------------------------------ SpMV
+def spmv(glob, layout, x, transpose: bool = False):
+    """The reference's distributed SpMV (spmv.hpp:149-169) restated
+    sequentially: split_matrix per rank, then the Csr loops in the reference
+    order (diag product, then += off-diagonal product; for the transpose
+    A^T x into zeros, B^T x into zeros, Reduce(SUM) into the owners in
+    ascending rank order, ops.cpp:364,372-376). Pure-Python loops: test-sized
+    matrices only. `glob` is a paper_2102_13018_b200.spmv.Csr."""
+    import numpy as np
+
+    from paper_2102_13018_b200 import spmv as S
+
+    P = layout.nranks()
+    ms = [S.split_matrix(glob, layout, layout, r) for r in range(P)]
+    ys = []
+    if not transpose:
+        for r, m in enumerate(ms):
+            xo = x[layout.begin(r):layout.end(r)]
+            y = m.diag.multiply(xo)
+            m.offdiag.multiply_add(x[m.garray], y)
+            ys.append(y)
+        return np.concatenate(ys)
+    lvecs = []
+    for r, m in enumerate(ms):
+        xo = x[layout.begin(r):layout.end(r)]
+        y = np.zeros(layout.local_size(r), dtype=glob.vals.dtype)
+        m.diag.multiply_transpose_add(xo, y)
+        lv = np.zeros(len(m.garray), dtype=glob.vals.dtype)
+        m.offdiag.multiply_transpose_add(xo, lv)
+        ys.append(y)
+        lvecs.append(lv)
+    with np.errstate(over="ignore"):
+        for r in range(P):  # owners fold remote contributions rank by rank
+            for s in range(P):
+                if s == r:
+                    continue
+                g = ms[s].garray
+                mine = (g >= layout.begin(r)) & (g < layout.end(r))
+                for gi, v in zip(g[mine], lvecs[s][mine]):
+                    ys[r][gi - layout.begin(r)] = ys[r][gi - layout.begin(r)] + v
+    return np.concatenate(ys)

@@ -40,6 +40,7 @@ def _load():
         lib.sfref_last_error.restype = C.c_char_p
         lib.sfref_rng.argtypes = [C.c_uint64, I64, V, C.c_uint64, V]
         lib.sfref_random_graph.argtypes = [C.c_uint64, I, I64, V, I64]
+        lib.sfref_spmv.argtypes = [I, I64, V, V, V, I, I, V, V]
         _lib = lib
     return _lib
 
@@ -167,3 +168,21 @@ def time_op(specs, opkind: str, dtype: str, op: str, steps: int, warmup: int = 1
     if rc != 0:
         raise RuntimeError(lib.sfref_last_error().decode())
     return {"setup_s": float(out[0]), "us_per_call": float(out[1])}
+
+
+def spmv(nranks: int, rowptr, colind, vals, x, transpose: bool = False) -> np.ndarray:
+    """The reference's distributed spmv / spmv_transpose (spmv.hpp:147-169)
+    over `nranks` rank threads with contiguous layouts, as selfcheck.cpp's
+    spmv_trial runs it; returns the concatenated y."""
+    lib = _load()
+    rowptr = np.ascontiguousarray(rowptr, np.int64)
+    colind = np.ascontiguousarray(colind, np.int64)
+    vals = np.ascontiguousarray(vals)
+    x = np.ascontiguousarray(x, vals.dtype)
+    n = len(rowptr) - 1
+    y = np.zeros(n, vals.dtype)
+    rc = lib.sfref_spmv(nranks, n, rowptr.ctypes.data, colind.ctypes.data, vals.ctypes.data,
+                        KIND[vals.dtype], int(transpose), x.ctypes.data, y.ctypes.data)
+    if rc != 0:
+        raise RuntimeError(lib.sfref_last_error().decode())
+    return y

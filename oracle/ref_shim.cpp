@@ -21,6 +21,7 @@
 #include "sf/harness.hpp"
 #include "sf/rng.hpp"
 #include "sf/ops.hpp"
+#include "sf/spmv.hpp"
 #include "sf/starforest.hpp"
 
 namespace {
@@ -274,3 +275,60 @@ int sfref_random_graph(uint64_t seed, int nranks, int64_t maxv, int64_t* out, in
 }
 
 }  // extern "C"
+
+namespace {
+// spmv_trial's distributed part (selfcheck.cpp:684-723): contiguous row and
+// column layouts, split_matrix, build_ghost_sf, spmv / spmv_transpose per
+// rank thread; y concatenated in rank order.
+template <class T>
+void spmv_run(int nranks, int64_t n, const int64_t* rowptr, const int64_t* colind, const T* vals,
+              int transpose, const T* x, T* y) {
+  sf::Csr<T> g;
+  g.rows = n;
+  g.cols = n;
+  g.rowptr.assign(rowptr, rowptr + n + 1);
+  g.colind.assign(colind, colind + rowptr[n]);
+  g.vals.assign(vals, vals + rowptr[n]);
+  const sf::Layout layout = sf::Layout::contiguous(n, nranks);
+  sf::RunConfig cfg;
+  cfg.nranks = nranks;
+  cfg.timeout_s = 60.0;
+  auto pieces = sf::run_ranks(cfg, [&](sf::Comm& comm) {
+    const int me = comm.rank();
+    auto m = sf::split_matrix(g, layout, layout, me);
+    sf::StarForest forest = sf::build_ghost_sf(comm, m);
+    sf::GhostVector<T> gx;
+    gx.owned.assign(x + layout.begin(me), x + layout.end(me));
+    gx.lvec.assign(m.garray.size(), T{});
+    std::vector<T> yy(static_cast<size_t>(layout.local_size(me)), T{});
+    if (!transpose)
+      sf::spmv(m, forest, gx, yy);
+    else
+      sf::spmv_transpose(m, forest, gx, yy);
+    return yy;
+  });
+  size_t k = 0;
+  for (const auto& p : pieces)
+    for (T v : p) y[k++] = v;
+}
+}  // namespace
+
+extern "C" {
+// kind: 1 int64, 2 float64 (sfg_kind numbering)
+int sfref_spmv(int nranks, int64_t n, const int64_t* rowptr, const int64_t* colind, const void* vals,
+               int kind, int transpose, const void* x, void* y) {
+  try {
+    if (kind == 2)
+      spmv_run<double>(nranks, n, rowptr, colind, static_cast<const double*>(vals), transpose,
+                       static_cast<const double*>(x), static_cast<double*>(y));
+    else
+      spmv_run<int64_t>(nranks, n, rowptr, colind, static_cast<const int64_t*>(vals), transpose,
+                        static_cast<const int64_t*>(x), static_cast<int64_t*>(y));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+}  // extern "C"
+

@@ -111,6 +111,10 @@ _SIGS = {
     "sfg_gather_end": (C.c_int, [_V]),
     "sfg_scatter_begin": (C.c_int, [_V, C.c_int, C.c_int64, _V, _V, _V, C.POINTER(_V)]),
     "sfg_scatter_end": (C.c_int, [_V]),
+    "sfg_mat_create": (C.c_int, [_V, C.c_int64, C.c_int64, _V, _V, _V, C.c_int, C.POINTER(_V)]),
+    "sfg_mat_destroy": (C.c_int, [_V]),
+    "sfg_spmv": (C.c_int, [_V, _V, _V, _V, _V, _V, _V]),
+    "sfg_spmv_transpose": (C.c_int, [_V, _V, _V, _V, _V, _V, _V]),
     "sfg_handle_info": (C.c_int, [_V, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "sfg_handle_free": (C.c_int, [_V]),
     "sfg_pattern_analyze": (C.c_int, [_V, C.c_int64, C.c_int, C.c_int64, C.c_int64,

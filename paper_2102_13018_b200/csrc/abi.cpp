@@ -16,6 +16,7 @@ struct sfg_comm_s {
   std::unique_ptr<sfg::Comm> c;
 };
 struct sfg_sf_s {};      // alias of sfg::StarForest
+struct sfg_mat_s {};     // alias of sfg::DevMatrix
 struct sfg_handle_s {};  // alias of sfg::OpHandle
 
 namespace {
@@ -372,6 +373,32 @@ int sfg_fetch_and_op_begin(sfg_sf sf, int kind, int64_t blocklen, void* rootdata
 }
 int sfg_fetch_and_op_end(sfg_handle h) {
   return guard([&] { sfg::fetch_and_op_end(*H(h)); });
+}
+
+int sfg_mat_create(sfg_comm c, int64_t rows, int64_t cols, const int64_t* rowptr,
+                   const int64_t* colind, const void* vals, int kind, sfg_mat* out) {
+  return guard([&] {
+    SFG_REQUIRE(c != nullptr, "matrix needs a valid communicator");
+    auto m = sfg::matrix_upload(*c->c, rows, cols, rowptr, colind, vals, unit(kind, 1).kind);
+    *out = reinterpret_cast<sfg_mat>(m.release());
+  });
+}
+int sfg_mat_destroy(sfg_mat m) {
+  return guard([&] { delete reinterpret_cast<sfg::DevMatrix*>(m); });
+}
+int sfg_spmv(sfg_sf sf, sfg_mat diag, sfg_mat offdiag, const void* x_owned, void* lvec, void* y,
+             void* stream) {
+  return guard([&] {
+    sfg::spmv(*SF(sf), *reinterpret_cast<sfg::DevMatrix*>(diag), *reinterpret_cast<sfg::DevMatrix*>(offdiag),
+              x_owned, lvec, y, st(stream));
+  });
+}
+int sfg_spmv_transpose(sfg_sf sf, sfg_mat diag, sfg_mat offdiag, const void* x_owned, void* lvec,
+                       void* y, void* stream) {
+  return guard([&] {
+    sfg::spmv_transpose(*SF(sf), *reinterpret_cast<sfg::DevMatrix*>(diag),
+                        *reinterpret_cast<sfg::DevMatrix*>(offdiag), x_owned, lvec, y, st(stream));
+  });
 }
 
 int sfg_gather_begin(sfg_sf sf, int kind, int64_t blocklen, const void* leafdata,

@@ -430,26 +430,34 @@ void end_wait(OpHandle& h, uint64_t tag, const std::vector<XferOp>& recvs) {
 // scatter runs on the caller's stream while the puts run on the comm stream.
 bool use_p2p(const OpHandle& h) { return h.sf->comm().p2p() && h.stg && h.stg->flags; }
 
+// The puts always run on the comm stream, so whatever the caller enqueues on
+// its stream between Begin and End (the local scatter, or its own work, e.g.
+// the diagonal SpMV product) overlaps the exchange; a small local scatter
+// joins the puts' launch instead.
 void p2p_begin(OpHandle& h, Launch& pack, Launch& local) {
   Comm& c = h.sf->comm();
   h.xfer = pack.p.nseg > 0;
-  const bool fuse = !h.xfer || local.algorithmic_bytes(h.unit) < kFuseLocalBytes;
-  if (fuse) {
+  h.forked = false;
+  if (!h.xfer) {
+    local.tag = tag_of(h, 0);
+    local.run(h.unit, h.op, h.stream);
+    return;
+  }
+  cudaStream_t cs = c.comm_stream();
+  c.fork(h.stream);
+  h.forked = true;
+  if (local.algorithmic_bytes(h.unit) < kFuseLocalBytes) {
     for (int i = 0; i < local.p.nseg; ++i)
       pack.add(local.p.seg[i], local.csr_entries[i], local.distinct_src[i], local.distinct_dst[i]);
     pack.tag = tag_of(h, 0);
-    pack.run(h.unit, h.op, h.stream);
-    h.forked = false;
+    pack.run(h.unit, h.op, cs);
   } else {
-    cudaStream_t cs = c.comm_stream();
-    c.fork(h.stream);
     pack.tag = tag_of(h, 2);
     local.tag = tag_of(h, 3);
     pack.run(h.unit, h.op, cs);
     local.run(h.unit, h.op, h.stream);
-    h.forked = true;
   }
-  if (h.xfer) counters().transport_calls++;
+  counters().transport_calls++;
 }
 
 // Before the unpack: order the caller's stream after this rank's own puts

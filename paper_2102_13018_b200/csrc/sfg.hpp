@@ -483,4 +483,31 @@ void scatter_end(OpHandle& h);
 
 DPat to_dpat(const Pattern& p, const int32_t* dev_idx);
 
+// ------------------------------------------------------- SpMV consumer
+// Device matrix block for the distributed SpMV (spmv.cu; reference
+// Csr<T> / SplitMatrix<T>, spmv.hpp:31-127): SELL-32 images of the block
+// and of its transpose.
+struct DevMatrix {
+  struct Sell {
+    int64_t rows = 0, cols = 0, nnz = 0, slots = 0;
+    int64_t* slice_off = nullptr;
+    int32_t* slice_w = nullptr;
+    int32_t* row_len = nullptr;
+    int32_t* col = nullptr;
+    void* val = nullptr;
+  };
+  int device = -1;
+  Kind kind = Kind::float64;
+  int64_t rows = 0, cols = 0, nnz = 0;
+  Sell fwd, bwd;  // the block and its transpose
+  std::vector<void*> allocs;
+  ~DevMatrix();
+};
+std::unique_ptr<DevMatrix> matrix_upload(Comm& comm, int64_t rows, int64_t cols, const int64_t* rowptr,
+                                         const int64_t* colind, const void* vals, Kind kind);
+void spmv(StarForest& sf, const DevMatrix& diag, const DevMatrix& off, const void* x_owned, void* lvec,
+          void* y, cudaStream_t s);
+void spmv_transpose(StarForest& sf, const DevMatrix& diag, const DevMatrix& off, const void* x_owned,
+                    void* lvec, void* y, cudaStream_t s);
+
 }  // namespace sfg

@@ -157,6 +157,24 @@ def test_p2p_stress_visibility():
 
 
 @need2
+def test_spmv_on_distinct_gpus_p2p():
+    """The SpMV consumer over the one-sided transport: ghost Bcast (forward)
+    and Reduce (transpose) between GPUs, bit-exact vs the oracle."""
+    from paper_2102_13018_b200 import spmv as S
+    from tests.test_cpu_spmv import trial
+    from tests.test_gpu_spmv import run_spmv
+
+    n = min(ngpu(), 4)
+    for t in range(4):
+        _, A, x = trial(t)
+        layout = S.Layout.contiguous(A.rows, n)
+        for transpose in (False, True):
+            got = run_spmv(A, layout, x, transpose, backend="p2p", devices=list(range(n)))
+            want = O.spmv(A, layout, x, transpose)
+            assert np.array_equal(got.view(np.int64), want.view(np.int64)), (t, transpose)
+
+
+@need2
 def test_p2p_needs_one_gpu_per_rank():
     import torch
 
