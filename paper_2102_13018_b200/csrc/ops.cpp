@@ -569,8 +569,12 @@ void end_root_to_leaf(OpHandle& h) {
   Launch L;
   L.tag = tag_of(h, 1);
   set_bufs(L, h, const_cast<void*>(h.src), h.dst, h.src);
+  // Remote leaves are disjoint from the self-edge leaves (each leaf has one
+  // root), so the unpack runs on the comm stream right behind the exchange,
+  // concurrently with a local scatter still running on the caller's stream;
+  // the caller's stream then joins.
+  Comm& c = sf.comm();
   if (use_p2p(h)) {
-    p2p_join(h);
     const auto bits = add_receives(h, L, d.rg, 0, true);
     for (size_t k = 0; k < d.rg.size(); ++k) {
       const auto& g = d.rg[k];
@@ -579,17 +583,23 @@ void end_root_to_leaf(OpHandle& h) {
       L.add(s);
       counters().unpack_copies++;
     }
-    L.run(h.unit, h.op, h.stream);
+    L.run(h.unit, h.op, h.forked ? c.comm_stream() : h.stream);
+    p2p_join(h);
     return;
   }
-  end_wait(h, data_tag(h.opid), h.recvs);
   for (size_t k = 0; k < d.rg.size(); ++k) {
     if (h.zero_copy_recv[k]) continue;
     const auto& g = d.rg[k];
     L.add(pair_seg(contig(g.stage_off), BUF_LEAF_STAGE, g.pat, BUF_LEAF, g.n, replace));
     counters().unpack_copies++;
   }
-  L.run(h.unit, h.op, h.stream);
+  if (h.xfer) {
+    c.transport().finish(data_tag(h.opid), h.recvs, c.comm_stream());
+    L.run(h.unit, h.op, c.comm_stream());
+    c.join(h.stream);
+  } else {
+    L.run(h.unit, h.op, h.stream);
+  }
 }
 
 // ---------------------------------------------------------- leaf -> root
