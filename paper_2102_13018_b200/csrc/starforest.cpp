@@ -12,6 +12,9 @@
 // descriptors only) plus, when a reduction needs it, a root-sorted CSR that
 // reproduces the reference's deterministic fold order.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -21,6 +24,19 @@ namespace sfg {
 
 namespace {
 constexpr int64_t kI32Max = (int64_t(1) << 31) - 1;
+
+// SFG_TRACE_SETUP=1 prints the wall time of each SetUp phase to stderr.
+struct PhaseTimer {
+  bool on = std::getenv("SFG_TRACE_SETUP") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[setup] %-28s %8.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
 
 // Id of the stream capture `s` takes part in, 0 when it is not capturing.
 unsigned long long capture_id(cudaStream_t s) {
@@ -133,6 +149,7 @@ void StarForest::setup(SetupAlg alg) {
   const int me = comm_->rank();
   const int P = comm_->size();
   const int64_t n = nleaves_;
+  PhaseTimer pt;
 
   // Edge order within a neighbor pair: ascending leaf index (starforest.cpp:86-90).
   std::vector<int64_t> order;
@@ -163,6 +180,7 @@ void StarForest::setup(SetupAlg alg) {
   }
   order.clear();
   order.shrink_to_fit();
+  pt.mark("order + group by rank");
 
   // Discovery payload: root offsets in edge order (starforest.cpp:96-107).
   std::vector<std::vector<uint8_t>> send(static_cast<size_t>(P));
@@ -173,7 +191,9 @@ void StarForest::setup(SetupAlg alg) {
     auto* p = reinterpret_cast<int64_t*>(buf.data());
     for (size_t i = 0; i < os.size(); ++i) p[i] = remote_off_[static_cast<size_t>(os[i])];
   }
+  pt.mark("payload");
   auto recv = comm_->ctrl().alltoallv(std::move(send));
+  pt.mark("discovery exchange");
 
   std::vector<Group> roots, leaves;
   for (int r = 0; r < P; ++r) {
@@ -200,6 +220,7 @@ void StarForest::setup(SetupAlg alg) {
     leaves.push_back(std::move(g));
   }
   recv.clear();
+  pt.mark("receive + validate");
   auto self_to_head = [me](std::vector<Group>& gs) {
     auto it = std::find_if(gs.begin(), gs.end(), [me](const Group& g) { return g.rank == me; });
     if (it != gs.end()) std::rotate(gs.begin(), it, it + 1);
@@ -213,7 +234,9 @@ void StarForest::setup(SetupAlg alg) {
     for (size_t i = 0; i < g.items.size(); ++i) leaf_idx[i] = leaf_index(g.items[i]);
     g.pat = Pattern::analyze(leaf_idx.data(), static_cast<int64_t>(leaf_idx.size()));
   }
+  pt.mark("analyze root groups");
   for (auto& g : leaves) g.pat = Pattern::analyze(g.items.data(), static_cast<int64_t>(g.items.size()));
+  pt.mark("analyze leaf groups");
 
   root_groups_ = std::move(roots);
   leaf_groups_ = std::move(leaves);
