@@ -183,6 +183,10 @@ struct ItemMap {
   }
 };
 
+__device__ __forceinline__ bool skipped(const uint32_t* bits, int64_t v) {
+  return bits != nullptr && ((__ldg(bits + (v >> 5)) >> (v & 31)) & 1u);
+}
+
 // dst[dpat(i)] (op)= src[spat(i)] over this CTA's items.
 template <class T, int OP, bool ATOMIC>
 __device__ __forceinline__ void run_pair(const DSeg& s, const LaunchParams& P, int64_t blk) {
@@ -202,7 +206,11 @@ __device__ __forceinline__ void run_pair(const DSeg& s, const LaunchParams& P, i
       int64_t i, k;
       im.split(e, i, k);
       const int64_t si = pat_index(s.src, i) * P.bl + k;
-      di[u] = pat_index(s.dst, i) * P.bl + k;
+      const int64_t dv = pat_index(s.dst, i);
+      if constexpr (OP != OP_REPLACE) {
+        if (skipped(s.skip_dst, dv)) continue;
+      }
+      di[u] = dv * P.bl + k;
       v[u] = src[si];
       if constexpr (OP != OP_REPLACE && !ATOMIC) d[u] = dst[di[u]];
     }
@@ -243,7 +251,8 @@ __device__ __forceinline__ void run_pair_rows(const DSeg& s, const LaunchParams&
     const int64_t in_run = pos - static_cast<int64_t>(r) * s.run;
     const int64_t len = min((s.run - in_run) * bl - k, wend - e);
     const T* sp = src + pat_index(s.src, pos) * bl + k;
-    T* dp = dst + pat_index(s.dst, pos) * bl + k;
+    const int64_t d0 = pat_index(s.dst, pos) * bl + k;  // element index of dp[0]
+    T* dp = dst + d0;
     T v[kItems];
     T d[kItems];
 #pragma unroll
@@ -254,10 +263,37 @@ __device__ __forceinline__ void run_pair_rows(const DSeg& s, const LaunchParams&
         if constexpr (OP != OP_REPLACE && !ATOMIC) d[u] = dp[i];
       }
     }
+    // Coupled roots (skip_dst): one bitmap word per lane covers the whole run
+    // (<= 32 * kItems vertices, bl == 1); only runs that contain a coupled
+    // root test their elements, the others store unconditionally.
+    uint32_t skipw = 0;
+    bool any_skip = false;
+    int64_t w0 = 0;
+    if constexpr (OP != OP_REPLACE) {
+      if (s.skip_dst != nullptr) {
+        if (bl == 1) {
+          w0 = d0 >> 5;
+          const int64_t w1 = (d0 + len - 1) >> 5;
+          if (w0 + lane <= w1) skipw = __ldg(s.skip_dst + w0 + lane);
+          any_skip = __any_sync(0xffffffffu, skipw != 0);
+        } else {
+          any_skip = true;
+        }
+      }
+    }
 #pragma unroll
     for (int u = 0; u < kItems; ++u) {
       const int64_t i = lane + 32 * u;
-      if (i < len) {
+      bool keep = i < len;
+      if constexpr (OP != OP_REPLACE) {
+        if (any_skip) {
+          const int64_t vx = bl == 1 ? d0 + i : (d0 + i) / bl;
+          const uint32_t word = bl == 1 ? __shfl_sync(0xffffffffu, skipw, static_cast<int>((vx >> 5) - w0) & 31)
+                                        : __ldg(s.skip_dst + (vx >> 5));
+          keep = keep && !((word >> (vx & 31)) & 1u);
+        }
+      }
+      if (keep) {
         if constexpr (OP == OP_REPLACE)
           dp[i] = v[u];
         else if constexpr (ATOMIC)
@@ -332,6 +368,7 @@ __device__ __forceinline__ void run_csr(const DSeg& s, const LaunchParams& P, in
     if (t0 >= total) return;
     int64_t r, k;
     im.split(t0, r, k);
+    if (skipped(s.skip_dst, __ldg(s.csr_roots + r))) return;
     const int32_t lo = __ldg(s.csr_lo + r);
     const int32_t hi = __ldg(s.csr_hi + r);
     if (lo >= hi) return;
@@ -343,6 +380,7 @@ __device__ __forceinline__ void run_csr(const DSeg& s, const LaunchParams& P, in
     for (int64_t e = t0; e < total; e += s.csr_grid_threads) {
       int64_t r, k;
       im.split(e, r, k);
+      if (skipped(s.skip_dst, __ldg(s.csr_roots + r))) continue;
       int32_t lo, hi;
       csr_piece(s, r, q, lo, hi);
       if (lo >= hi) continue;
@@ -450,6 +488,7 @@ __device__ __forceinline__ void run_csr_warp(const DSeg& s, const LaunchParams& 
     if (w0 >= items) return;
     int64_t r, k;
     im.split(w0, r, k);
+    if (skipped(s.skip_dst, __ldg(s.csr_roots + r))) return;
     const int32_t lo = __ldg(s.csr_lo + r);
     const int32_t hi = __ldg(s.csr_hi + r);
     if (lo >= hi) return;
@@ -463,6 +502,7 @@ __device__ __forceinline__ void run_csr_warp(const DSeg& s, const LaunchParams& 
     for (int64_t w = w0; w < items; w += nw) {
       int64_t r, k;
       im.split(w, r, k);
+      if (skipped(s.skip_dst, __ldg(s.csr_roots + r))) continue;
       int32_t lo, hi;
       csr_piece(s, r, q, lo, hi);
       if (lo >= hi) continue;

@@ -120,6 +120,9 @@ struct DSeg {
   // Counters live in device memory, so a captured CUDA graph replays the
   // protocol correctly.
   uint32_t wait_mask = 0;
+  // Reductions: destination roots whose bit is set are left alone (their
+  // whole fold runs in another launch, see DevPlan::coupled_bits).
+  const uint32_t* skip_dst = nullptr;
   unsigned int* sig_count = nullptr;
   unsigned long long* sig_flag = nullptr;
   unsigned long long* sig_seq = nullptr;

@@ -345,6 +345,21 @@ bool prefer_csr(StarForest& sf, bool det, CsrRange range) {
   return true;
 }
 
+// Reduce with self edges and remote contributions: Begin's local reduction
+// skips the "coupled" roots (those that also receive remote contributions)
+// and End folds them completely — self entries then remote ranks, the
+// reference order — from the full CSR. The local reduction and the End fold
+// then touch disjoint roots, so the End fold runs on the comm stream right
+// behind the exchange while the local reduction is still running.
+bool split_coupled(StarForest& sf, const OpHandle& h) {
+  const DevPlan& d = sf.dev();
+  if (h.op == ReduceOp::replace || !d.has_self || d.lg.empty()) return false;
+  static const bool off = std::getenv("SFG_NO_COUPLED_SPLIT") != nullptr;
+  if (off) return false;
+  sf.ensure_csr();
+  return d.coupled_bits != nullptr && d.ccsr_lo != nullptr && d.rcsr_n > 0;
+}
+
 // Exact sequential order is only needed for floating point; integer ops are
 // associative under wrap-around, so tree/scan orders give identical bits.
 bool exact_seq(const OpHandle& h, bool det) { return det && h.unit.kind == Kind::float64; }
@@ -641,6 +656,9 @@ void begin_leaf_to_root(OpHandle& h) {
                 d.self_root_distinct);
     }
   }
+  h.coupled_split = split_coupled(sf, h);
+  if (h.coupled_split)
+    for (int i = 0; i < local.p.nseg; ++i) local.p.seg[i].skip_dst = d.coupled_bits;
   if (p2p) {
     p2p_begin(h, pack, local);
     return;
@@ -667,6 +685,30 @@ void end_leaf_to_root(OpHandle& h) {
   L.tag = tag_of(h, 1);
   set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
   std::vector<uint32_t> bits(d.lg.size(), 0);
+  Comm& c = sf.comm();
+  if (h.coupled_split) {
+    // Whole fold of the coupled roots, concurrent with Begin's local part.
+    const bool p2p = use_p2p(h);
+    if (p2p) bits = add_receives(h, L, d.lg, 1, true);
+    DSeg s = csr_seg(d, CsrRange::remote_only, SEG_CSR_FOLD, exact_seq(h, det), h.unit.bytes());
+    s.csr_lo = d.ccsr_lo;
+    s.csr_hi = d.ccsr_hi;
+    s.csr_ent = d.csr_ent;
+    for (uint32_t b : bits) s.wait_mask |= b;
+    L.add(s, d.ccsr_entries);
+    counters().unpack_copies += d.lg.size();
+    if (p2p) {
+      L.run(h.unit, h.op, h.forked ? c.comm_stream() : h.stream);
+      p2p_join(h);
+    } else if (h.xfer) {
+      c.transport().finish(data_tag(h.opid), h.recvs, c.comm_stream());
+      L.run(h.unit, h.op, c.comm_stream());
+      c.join(h.stream);
+    } else {
+      L.run(h.unit, h.op, h.stream);
+    }
+    return;
+  }
   if (use_p2p(h)) {
     p2p_join(h);
     bits = add_receives(h, L, d.lg, 1, true);

@@ -323,6 +323,15 @@ struct DevPlan {
   int32_t* rcsr_roots = nullptr;
   int32_t* rcsr_off = nullptr;  // [rcsr_n + 1]
   int32_t* rcsr_ent = nullptr;
+  // "coupled" roots (self AND remote contributions): their whole fold (self
+  // entries then remote, the reference order) runs in End from the full CSR
+  // (ccsr_lo/hi index csr_ent, aligned with rcsr_roots); Begin's local
+  // reduction skips them (coupled_bits, one bit per root), so it can run
+  // concurrently with the exchange and the End fold.
+  int32_t* ccsr_lo = nullptr;
+  int32_t* ccsr_hi = nullptr;
+  uint32_t* coupled_bits = nullptr;
+  int64_t ccsr_entries = 0;
   ~DevPlan();
 };
 
@@ -455,6 +464,7 @@ struct OpHandle {
   std::vector<XferOp> recvs;        // phase-1 receives
   std::vector<XferOp> reply_recvs;  // fetch-and-op replies
   bool forked = false;              // p2p: the puts ran on the comm stream
+  bool coupled_split = false;       // reduce: coupled roots folded in End (DevPlan::coupled_bits)
   std::vector<uint8_t> zero_copy_recv;
   // debug checksum
   const void* ck_ptr = nullptr;

@@ -478,19 +478,28 @@ void StarForest::ensure_csr() {
 
   // Remote-only view: the (usually few) roots with remote contributions, so
   // the End-side fold does not walk every root of the forest.
-  std::vector<int32_t> rroots, roffs, rent;
+  std::vector<int32_t> rroots, roffs, rent, clo, chi;
+  std::vector<uint32_t> cbits;
+  if (self) cbits.assign(static_cast<size_t>((nroots_ + 31) / 32), 0u);
   for (size_t q = 0; q < roots.size(); ++q) {
     const int32_t a = split[q], b = offs[q + 1];
     if (a == b) continue;
     rroots.push_back(roots[q]);
     roffs.push_back(static_cast<int32_t>(rent.size()));
     rent.insert(rent.end(), ent.begin() + a, ent.begin() + b);
+    if (self) {
+      clo.push_back(offs[q]);
+      chi.push_back(b);
+      d.ccsr_entries += b - offs[q];
+      if (a > offs[q]) cbits[static_cast<size_t>(roots[q]) >> 5] |= 1u << (roots[q] & 31);
+    }
   }
   roffs.push_back(static_cast<int32_t>(rent.size()));
   d.rcsr_n = static_cast<int64_t>(rroots.size());
 
   const size_t bytes = (roots.size() + offs.size() + split.size() + ent.size() + rroots.size() +
-                        roffs.size() + rent.size() + ptab.size()) * sizeof(int32_t);
+                        roffs.size() + rent.size() + ptab.size() + clo.size() + chi.size() +
+                        cbits.size()) * sizeof(int32_t);
   if (bytes) {
     SFG_CUDA(cudaMalloc(&d.csr_blob, bytes));
     auto* p = static_cast<int32_t*>(d.csr_blob);
@@ -508,6 +517,12 @@ void StarForest::ensure_csr() {
     put(rent, d.rcsr_ent);
     put(ptab, d.csr_ptab);
     if (ptab.empty()) d.csr_ptab = nullptr;
+    put(clo, d.ccsr_lo);
+    put(chi, d.ccsr_hi);
+    std::vector<int32_t> cb(cbits.begin(), cbits.end());
+    int32_t* cbp = nullptr;
+    put(cb, cbp);
+    d.coupled_bits = cbits.empty() ? nullptr : reinterpret_cast<uint32_t*>(cbp);
   }
   d.csr_built = true;
 }

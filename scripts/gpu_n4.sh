@@ -2,6 +2,4 @@ O=gpurun_out; mkdir -p $O
 timeout 900 python -m pytest tests/test_gpu_multi.py -x -q > $O/multi_n4.log 2>&1
 for t in p2p nccl; do
 timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29541 bench.py --gpus 4 --transport $t > $O/bench_n4_$t.log 2>&1
-timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29542 bench.py --gpus 2 --transport $t > $O/bench_n2_$t.log 2>&1
 done
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29543 bench_configs.py --config 3 --spmv > $O/cfg3_spmv_n4.log 2>&1
