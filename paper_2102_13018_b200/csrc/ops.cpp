@@ -3,23 +3,26 @@
 // Reference engines: /root/reference/proj/src/ops.cpp
 //   root->leaf two-sided  :276-324   (bcast, scatter)
 //   leaf->root two-sided  :326-376   (reduce, gather)
+//   one-sided engines     :160-246, 381-476, 572-658 (the p2p backend here)
 //   fetch-and-op          :481-570
 //   public begin/end      :697-876
-// Per Begin: ONE fused kernel launch packs every remote group whose pattern
-// is not contiguous and performs the local (self-edge) scatter, then ONE
-// grouped transport call posts all sends and receives on the caller's
-// stream. Per End: the transport's receives are ordered before ONE unpack
-// launch. Contiguous patterns are zero-copy on the send side, and on the
-// receive side when op == REPLACE (ops.cpp:289-291,339-341). Nothing
-// synchronises the host with the GPU (§V "stream-aware, sync-free").
+// Per Begin: the exchange is forked onto the communicator's stream — ONE
+// launch packs every remote group (p2p: straight into the peers' slots over
+// NVLink; nccl: into staging, then ONE grouped send/recv; contiguous groups
+// are zero-copy sends) — while the local (self-edge) scatter runs on the
+// caller's stream (or joins the pack launch when small). Per End: ONE unpack
+// launch (on the comm stream when it cannot conflict with the local scatter:
+// Bcast always, Reduce for the "coupled" roots), then the caller's stream
+// joins. Nothing synchronises the host with the GPU (§V
+// "stream-aware, sync-free").
 //
 // Fold order. Where a reduction can hit the same root more than once, the
-// deterministic mode (CommConfig::deterministic, the reference default) folds
-// through a root-sorted CSR in exactly the reference order — initial value,
-// self edges by ascending leaf index, then remote ranks ascending, each in
-// ascending leaf index (ops.cpp:364,372-376; oracle.cpp:84-90) — so
-// floating-point results are bit-identical to the CPU reference. The
-// free-order mode uses atomics (pack.cpp:47-58 "atomics" mode).
+// fold runs through a root-sorted CSR in exactly the reference order —
+// initial value, self edges by ascending leaf index, then remote ranks
+// ascending, each in ascending leaf index (ops.cpp:364,372-376;
+// oracle.cpp:84-90) — so floating-point results are bit-identical to the CPU
+// reference in both modes (free-order mode keeps an atomics path behind
+// SFG_FREE_ORDER_ATOMICS, pack.cpp:47-58 "atomics" mode).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>

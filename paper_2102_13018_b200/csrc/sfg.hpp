@@ -6,9 +6,10 @@
 //   StarForest (set_graph/setup/degrees/multi_sf) <- starforest.hpp
 //   split-phase operations                        <- ops.hpp
 // but the data plane is device-resident: per-peer plans live in HBM, packs
-// and unpacks are sm_100a kernels (kernels.cu), remote exchange is grouped
-// NCCL send/recv (or stream-ordered peer copies for in-process ranks), and
-// nothing synchronises the host between Begin and End.
+// and unpacks are sm_100a kernels (kernels.cu), remote exchange is one-sided
+// NVLink puts with in-kernel flags (p2p.cpp), grouped NCCL send/recv, or
+// stream-ordered peer copies for in-process ranks, and nothing synchronises
+// the host between Begin and End.
 #pragma once
 
 #include <cuda_runtime.h>

@@ -51,6 +51,35 @@ __global__ void put_kernel(const char* __restrict__ src, char* dst, size_t bytes
   }
 }
 
+// The library's shape: each thread stores E 8-byte elements (lane-strided
+// inside a warp's 32*E chunk), one completion flag per launch (mode 3).
+template <int E>
+__global__ void put_e_kernel(const unsigned long long* __restrict__ src, unsigned long long* dst, size_t n,
+                             unsigned long long* flag, unsigned int* count, unsigned long long value) {
+  const size_t warp_base = (blockIdx.x * (size_t)blockDim.x + (threadIdx.x & ~31u)) * E;
+  const unsigned lane = threadIdx.x & 31;
+  unsigned long long v[E];
+#pragma unroll
+  for (int u = 0; u < E; ++u) {
+    const size_t i = warp_base + lane + 32 * u;
+    if (i < n) v[u] = src[i];
+  }
+#pragma unroll
+  for (int u = 0; u < E; ++u) {
+    const size_t i = warp_base + lane + 32 * u;
+    if (i < n) dst[i] = v[u];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned prev;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(count) : "memory");
+    if (prev + 1 == gridDim.x) {
+      *count = 0;
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
+    }
+  }
+}
+
 __global__ void spin_then_signal(const unsigned long long* my_flag, unsigned long long want,
                                  unsigned long long* peer_flag, unsigned long long value) {
   if (threadIdx.x != 0) return;
@@ -124,7 +153,7 @@ int main() {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   unsigned long long seq = 0;
-  for (size_t bytes = 8; bytes <= maxb; bytes *= 4) {
+  for (size_t bytes = 2097152; bytes <= 2097152; bytes *= 4) {
     for (int w : {16}) {
       for (int fence : {0, 1, 2, 3}) {
         for (int grid_mode : {0}) {  // 0: 1 element per thread, 1: grid = 4 x SMs (grid-stride)
@@ -160,6 +189,42 @@ int main() {
           CK(cudaGraphDestroy(g));
         }
       }
+    }
+  }
+
+  // 2b. the library's per-thread element count
+  for (size_t bytes : {size_t(262144), size_t(2097152), size_t(8388608)}) {
+    const size_t n = bytes / 8;
+    for (int E : {1, 2, 4, 8}) {
+      const int grid = (int)((n + 256 * E - 1) / (256 * E));
+      const int reps = 20;
+      cudaGraph_t g;
+      cudaGraphExec_t ge;
+      CK(cudaStreamBeginCapture(s0, cudaStreamCaptureModeGlobal));
+      for (int r = 0; r < reps; ++r) {
+        ++seq;
+        auto* sp = reinterpret_cast<const unsigned long long*>(src0);
+        auto* dp = reinterpret_cast<unsigned long long*>(dst1);
+        if (E == 1) put_e_kernel<1><<<grid, 256, 0, s0>>>(sp, dp, n, flag1, cnt0, seq);
+        if (E == 2) put_e_kernel<2><<<grid, 256, 0, s0>>>(sp, dp, n, flag1, cnt0, seq);
+        if (E == 4) put_e_kernel<4><<<grid, 256, 0, s0>>>(sp, dp, n, flag1, cnt0, seq);
+        if (E == 8) put_e_kernel<8><<<grid, 256, 0, s0>>>(sp, dp, n, flag1, cnt0, seq);
+      }
+      CK(cudaStreamEndCapture(s0, &g));
+      CK(cudaGraphInstantiate(&ge, g, 0));
+      CK(cudaGraphLaunch(ge, s0));
+      CK(cudaStreamSynchronize(s0));
+      CK(cudaEventRecord(a, s0));
+      CK(cudaGraphLaunch(ge, s0));
+      CK(cudaEventRecord(b, s0));
+      CK(cudaEventSynchronize(b));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, a, b));
+      const double us = ms * 1e3 / reps;
+      std::printf("{\"test\": \"put_e\", \"bytes\": %zu, \"elems_per_thread\": %d, \"grid\": %d, \"us\": %.3f, \"GBps\": %.1f}\n",
+                  bytes, E, grid, us, bytes / (us * 1e-6) / 1e9);
+      CK(cudaGraphExecDestroy(ge));
+      CK(cudaGraphDestroy(g));
     }
   }
 
