@@ -165,6 +165,17 @@ int sfg_gather_end(sfg_handle h);
 int sfg_scatter_begin(sfg_sf sf, int kind, int64_t blocklen, const void* multirootdata,
                       void* leafdata, void* stream, sfg_handle* out);
 int sfg_scatter_end(sfg_handle h);
+/* Graph algebra (starforest.hpp:150-171). Collective over the operands'
+ * communicator; the new forest is set up (identity: graph set, as the
+ * reference's identity_sf). compose: roots of A, leaves of B, an edge where an
+ * A leaf and a B root coincide; inverse != 0: compose_inverse (leaves of AB =
+ * B's roots; B roots of degree <= 1, A's leaves covered by B's leaves).
+ * embed: which = 0 keeps edges whose root is in sel (validated against
+ * nroots), 1 edges whose leaf index is in sel (>= 0); indices not remapped. */
+int sfg_sf_compose(sfg_sf a, sfg_sf b, int inverse, sfg_sf* out);
+int sfg_sf_embed(sfg_sf sf, int which, const int64_t* sel, int64_t n, sfg_sf* out);
+int sfg_sf_identity(sfg_comm c, int64_t n, sfg_sf* out);
+
 /* Distributed SpMV over a ghost forest — the path's consumer
  * (spmv.hpp:147-169). A matrix block is uploaded once from host CSR arrays
  * (Csr<T>, spmv.hpp:31-78; kind SFG_FLOAT64 or SFG_INT64) to the

@@ -226,6 +226,12 @@ class StarForest {
   }
 
   sfg_sf handle() const { return h_; }
+  // Takes ownership of a forest the library created (graph algebra).
+  static StarForest adopt(sfg_sf owned) {
+    StarForest f(owned);
+    f.owned_ = true;
+    return f;
+  }
 
  private:
   explicit StarForest(sfg_sf borrowed) : h_(borrowed), owned_(false) {}
@@ -238,6 +244,34 @@ class StarForest {
   bool owned_ = true;
   std::unique_ptr<StarForest> multi_;
 };
+
+// --------------------------------------------------------- graph algebra
+// starforest.hpp:150-171
+inline StarForest compose(StarForest& a, StarForest& b) {
+  sfg_sf h = nullptr;
+  detail::check(sfg_sf_compose(a.handle(), b.handle(), 0, &h));
+  return StarForest::adopt(h);
+}
+inline StarForest compose_inverse(StarForest& a, StarForest& b) {
+  sfg_sf h = nullptr;
+  detail::check(sfg_sf_compose(a.handle(), b.handle(), 1, &h));
+  return StarForest::adopt(h);
+}
+inline StarForest embed_root(StarForest& f, const std::vector<std::int64_t>& selected) {
+  sfg_sf h = nullptr;
+  detail::check(sfg_sf_embed(f.handle(), 0, selected.data(), static_cast<std::int64_t>(selected.size()), &h));
+  return StarForest::adopt(h);
+}
+inline StarForest embed_leaf(StarForest& f, const std::vector<std::int64_t>& selected) {
+  sfg_sf h = nullptr;
+  detail::check(sfg_sf_embed(f.handle(), 1, selected.data(), static_cast<std::int64_t>(selected.size()), &h));
+  return StarForest::adopt(h);
+}
+inline StarForest identity_sf(Comm& c, std::int64_t n) {
+  sfg_sf h = nullptr;
+  detail::check(sfg_sf_identity(c.handle(), n, &h));
+  return StarForest::adopt(h);
+}
 
 // ------------------------------------------------------------ operations
 class OpHandle {

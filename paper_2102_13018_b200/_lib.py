@@ -111,6 +111,9 @@ _SIGS = {
     "sfg_gather_end": (C.c_int, [_V]),
     "sfg_scatter_begin": (C.c_int, [_V, C.c_int, C.c_int64, _V, _V, _V, C.POINTER(_V)]),
     "sfg_scatter_end": (C.c_int, [_V]),
+    "sfg_sf_compose": (C.c_int, [_V, _V, C.c_int, C.POINTER(_V)]),
+    "sfg_sf_embed": (C.c_int, [_V, C.c_int, _V, C.c_int64, C.POINTER(_V)]),
+    "sfg_sf_identity": (C.c_int, [_V, C.c_int64, C.POINTER(_V)]),
     "sfg_mat_create": (C.c_int, [_V, C.c_int64, C.c_int64, _V, _V, _V, C.c_int, C.POINTER(_V)]),
     "sfg_mat_destroy": (C.c_int, [_V]),
     "sfg_spmv": (C.c_int, [_V, _V, _V, _V, _V, _V, _V]),

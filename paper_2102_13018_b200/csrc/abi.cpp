@@ -375,6 +375,26 @@ int sfg_fetch_and_op_end(sfg_handle h) {
   return guard([&] { sfg::fetch_and_op_end(*H(h)); });
 }
 
+int sfg_sf_compose(sfg_sf a, sfg_sf b, int inverse, sfg_sf* out) {
+  return guard([&] {
+    auto f = inverse ? sfg::compose_inverse(*SF(a), *SF(b)) : sfg::compose(*SF(a), *SF(b));
+    *out = reinterpret_cast<sfg_sf>(f.release());
+  });
+}
+int sfg_sf_embed(sfg_sf sf, int which, const int64_t* sel, int64_t n, sfg_sf* out) {
+  return guard([&] {
+    SFG_REQUIRE(n == 0 || sel != nullptr, "embed: selection pointer is null");
+    auto f = which == 0 ? sfg::embed_root(*SF(sf), sel, n) : sfg::embed_leaf(*SF(sf), sel, n);
+    *out = reinterpret_cast<sfg_sf>(f.release());
+  });
+}
+int sfg_sf_identity(sfg_comm c, int64_t n, sfg_sf* out) {
+  return guard([&] {
+    SFG_REQUIRE(c != nullptr, "identity_sf needs a valid communicator");
+    *out = reinterpret_cast<sfg_sf>(sfg::identity_sf(*c->c, n).release());
+  });
+}
+
 int sfg_mat_create(sfg_comm c, int64_t rows, int64_t cols, const int64_t* rowptr,
                    const int64_t* colind, const void* vals, int kind, sfg_mat* out) {
   return guard([&] {

@@ -494,6 +494,15 @@ void scatter_end(OpHandle& h);
 
 DPat to_dpat(const Pattern& p, const int32_t* dev_idx);
 
+// ------------------------------------------------------- graph algebra
+// starforest.hpp:150-171 (algebra.cpp). Collective; results are set up
+// (identity_sf: graph set).
+std::unique_ptr<StarForest> compose(StarForest& A, StarForest& B);
+std::unique_ptr<StarForest> compose_inverse(StarForest& A, StarForest& B);
+std::unique_ptr<StarForest> embed_root(StarForest& f, const int64_t* sel, int64_t nsel);
+std::unique_ptr<StarForest> embed_leaf(StarForest& f, const int64_t* sel, int64_t nsel);
+std::unique_ptr<StarForest> identity_sf(Comm& c, int64_t n);
+
 // ------------------------------------------------------- SpMV consumer
 // Device matrix block for the distributed SpMV (spmv.cu; reference
 // Csr<T> / SplitMatrix<T>, spmv.hpp:31-127): SELL-32 images of the block

@@ -651,6 +651,52 @@ def timing_collect() -> dict:
             for i in range(n.value)}
 
 
+# ------------------------------------------------------------ graph algebra
+def _new_forest(comm: Comm, h: C.c_void_p) -> StarForest:
+    f = StarForest.__new__(StarForest)
+    f.comm, f._owned, f._h, f._multi = comm, True, h, None
+    return f
+
+
+def compose(a: StarForest, b: StarForest) -> StarForest:
+    """starforest.hpp:150-154 (collective): roots of A, leaves of B, an edge
+    where an A leaf and a B root coincide on (rank, index)."""
+    h = C.c_void_p()
+    _check(_lib().sfg_sf_compose(a._h, b._h, 0, C.byref(h)))
+    return _new_forest(a.comm, h)
+
+
+def compose_inverse(a: StarForest, b: StarForest) -> StarForest:
+    """starforest.hpp:156-159 (collective): roots of A, leaves = B's roots."""
+    h = C.c_void_p()
+    _check(_lib().sfg_sf_compose(a._h, b._h, 1, C.byref(h)))
+    return _new_forest(a.comm, h)
+
+
+def _embed(f: StarForest, which: int, selected) -> StarForest:
+    sel = np.ascontiguousarray(np.asarray(selected, dtype=np.int64))
+    h = C.c_void_p()
+    _check(_lib().sfg_sf_embed(f._h, which, sel.ctypes.data if sel.size else None, sel.size, C.byref(h)))
+    return _new_forest(f.comm, h)
+
+
+def embed_root(f: StarForest, selected_roots) -> StarForest:
+    """starforest.hpp:161-166: keep the edges whose root is selected."""
+    return _embed(f, 0, selected_roots)
+
+
+def embed_leaf(f: StarForest, selected_leaves) -> StarForest:
+    """starforest.hpp:161-167: keep the edges whose leaf index is selected."""
+    return _embed(f, 1, selected_leaves)
+
+
+def identity_sf(comm: Comm, n: int) -> StarForest:
+    """starforest.hpp:169-171: leaf i -> root i on this rank (graph set)."""
+    h = C.c_void_p()
+    _check(_lib().sfg_sf_identity(comm._h, n, C.byref(h)))
+    return _new_forest(comm, h)
+
+
 # ----------------------------------------------------------------- harness
 def run_ranks(cfg: CommConfig, body: Callable[[Comm], Any], devices: Optional[Sequence[int]] = None) -> list:
     """harness.hpp:58-72: one thread per rank, results per rank; a failing or

@@ -37,6 +37,7 @@ static void host_mode() {
   std::vector<std::vector<std::int64_t>> deg(3);
   std::vector<TwoSidedInfo> ti(3);
   std::vector<std::int64_t> multi(3);
+  std::vector<std::int64_t> embedded(3), composed(3);
   run_ranks(cfg, [&](Comm& c) {
     StarForest f(c);
     f.set_graph(specs[static_cast<std::size_t>(c.rank())]);
@@ -44,7 +45,16 @@ static void host_mode() {
     ti[static_cast<std::size_t>(c.rank())] = f.two_sided();
     deg[static_cast<std::size_t>(c.rank())] = f.compute_degrees();
     multi[static_cast<std::size_t>(c.rank())] = f.multi_sf().nroots();
+    // graph algebra (test_sfgraph.cpp:416-434, 266-284)
+    std::vector<std::int64_t> sel;
+    if (c.rank() == 1) sel.push_back(0);
+    embedded[static_cast<std::size_t>(c.rank())] = embed_root(f, sel).nleaves();
+    StarForest id = identity_sf(c, f.nroots());
+    id.setup();
+    composed[static_cast<std::size_t>(c.rank())] = compose(id, f).nleaves();
   }, {-1, -1, -1});
+  CHECK((embedded == std::vector<std::int64_t>{2, 0, 1}));
+  CHECK((composed == std::vector<std::int64_t>{4, 3, 3}));
   CHECK((deg[0] == std::vector<std::int64_t>{2, 0, 1}));
   CHECK((deg[1] == std::vector<std::int64_t>{3, 0, 1, 1}));
   CHECK((deg[2] == std::vector<std::int64_t>{1, 1}));
