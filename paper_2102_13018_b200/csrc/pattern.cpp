@@ -13,6 +13,7 @@
 #include <mutex>
 #include <sstream>
 
+#include "parallel.hpp"
 #include "sfg.hpp"
 
 namespace sfg {
@@ -200,17 +201,18 @@ int64_t count_distinct(const std::vector<int64_t>& v, int64_t lo, int64_t hi) {
   return static_cast<int64_t>(std::unique(sorted.begin(), sorted.end()) - sorted.begin());
 }
 
-// Verify start + k*s2 + j*s1 + x over (dz, dy, dx).
+// Verify start + k*s2 + j*s1 + x over (dz, dy, dx), rows in parallel.
 bool verify_affine(const int64_t* idx, int64_t start, int64_t dx, int64_t dy, int64_t dz,
                    int64_t s1, int64_t s2) {
-  int64_t p = 0;
-  for (int64_t k = 0; k < dz; ++k)
-    for (int64_t j = 0; j < dy; ++j) {
-      const int64_t row = start + k * s2 + j * s1;
-      for (int64_t x = 0; x < dx; ++x)
-        if (idx[p++] != row + x) return false;
-    }
-  return true;
+  const int64_t rows = dy * dz;
+  return parallel_find_first(rows, [&](int64_t r) {
+           const int64_t k = r / dy, j = r - k * dy;
+           const int64_t row = start + k * s2 + j * s1;
+           const int64_t* p = idx + r * dx;
+           for (int64_t x = 0; x < dx; ++x)
+             if (p[x] != row + x) return true;
+           return false;
+         }) == rows;
 }
 
 }  // namespace

@@ -18,6 +18,7 @@
 #include <cstring>
 #include <numeric>
 
+#include "parallel.hpp"
 #include "sfg.hpp"
 
 namespace sfg {
@@ -95,11 +96,10 @@ void StarForest::set_graph(int64_t nroots, int64_t nleaves, const int64_t* leaf_
   int64_t bound = nleaves;
   bool contiguous = true;
   if (leaf_local != nullptr) {
-    bool increasing = true;
-    for (int64_t i = 0; i < nleaves; ++i) {
-      if (i > 0 && leaf_local[i] <= leaf_local[i - 1]) increasing = false;
-      contiguous = contiguous && leaf_local[i] == i;
-    }
+    const bool increasing =
+        parallel_find_first(nleaves, [&](int64_t i) { return i > 0 && leaf_local[i] <= leaf_local[i - 1]; }) ==
+        nleaves;
+    contiguous = parallel_find_first(nleaves, [&](int64_t i) { return leaf_local[i] != i; }) == nleaves;
     if (increasing) {
       SFG_REQUIRE(nleaves == 0 || leaf_local[0] >= 0, "set_graph: negative leaf index");
       bound = nleaves == 0 ? 0 : leaf_local[nleaves - 1] + 1;
@@ -116,10 +116,13 @@ void StarForest::set_graph(int64_t nroots, int64_t nleaves, const int64_t* leaf_
     }
   }
   const int nranks = comm_->size();
-  for (int64_t i = 0; i < nleaves; ++i) {
-    SFG_REQUIRE(remote_rank[i] >= 0 && remote_rank[i] < nranks,
-                "set_graph: root rank " + std::to_string(remote_rank[i]) + " outside communicator");
-    SFG_REQUIRE(remote_off[i] >= 0, "set_graph: negative root offset");
+  const int64_t bad = parallel_find_first(nleaves, [&](int64_t i) {
+    return remote_rank[i] < 0 || remote_rank[i] >= nranks || remote_off[i] < 0;
+  });
+  if (bad < nleaves) {
+    SFG_REQUIRE(remote_rank[bad] >= 0 && remote_rank[bad] < nranks,
+                "set_graph: root rank " + std::to_string(remote_rank[bad]) + " outside communicator");
+    SFG_REQUIRE(remote_off[bad] >= 0, "set_graph: negative root offset");
   }
 
   nroots_ = nroots;
@@ -127,12 +130,18 @@ void StarForest::set_graph(int64_t nroots, int64_t nleaves, const int64_t* leaf_
   leaf_bound_ = bound;
   contiguous_leaves_ = contiguous;
   has_local_ = leaf_local != nullptr;
+  auto pcopy = [nleaves](auto& dst, const auto* src) {
+    dst.resize(static_cast<size_t>(nleaves));
+    parallel_chunks(nleaves, [&](int, int64_t b, int64_t e) {
+      std::copy(src + b, src + e, dst.begin() + b);
+    });
+  };
   if (has_local_ && !contiguous)
-    leaf_local_.assign(leaf_local, leaf_local + nleaves);
+    pcopy(leaf_local_, leaf_local);
   else
     leaf_local_.clear();  // identity: leaf index == ordinal
-  remote_rank_.assign(remote_rank, remote_rank + nleaves);
-  remote_off_.assign(remote_off, remote_off + nleaves);
+  pcopy(remote_rank_, remote_rank);
+  pcopy(remote_off_, remote_off);
   root_groups_.clear();
   leaf_groups_.clear();
   self_first_ = false;
@@ -167,30 +176,54 @@ void StarForest::setup(SetupAlg alg) {
   }
   auto ord = [&](int64_t i) { return identity ? i : order[static_cast<size_t>(i)]; };
 
-  // Group by root rank, ascending, stable (counting sort).
-  std::vector<int64_t> cnt(static_cast<size_t>(P) + 1, 0);
-  for (int64_t i = 0; i < n; ++i) ++cnt[static_cast<size_t>(remote_rank_[static_cast<size_t>(i)]) + 1];
-  for (int r = 0; r < P; ++r) cnt[static_cast<size_t>(r) + 1] += cnt[static_cast<size_t>(r)];
+  // Group by root rank, ascending, stable (counting sort, per-chunk counts
+  // so the threads scatter in order).
+  const int nc = chunk_count(n);
+  std::vector<std::vector<int64_t>> ccnt(static_cast<size_t>(nc), std::vector<int64_t>(static_cast<size_t>(P), 0));
+  parallel_chunks(n, [&](int c, int64_t b, int64_t e) {
+    auto& k = ccnt[static_cast<size_t>(c)];
+    for (int64_t i = b; i < e; ++i) ++k[static_cast<size_t>(remote_rank_[static_cast<size_t>(ord(i))])];
+  });
   std::vector<std::vector<int64_t>> ords(static_cast<size_t>(P));
-  for (int r = 0; r < P; ++r)
-    ords[static_cast<size_t>(r)].reserve(static_cast<size_t>(cnt[static_cast<size_t>(r) + 1] - cnt[static_cast<size_t>(r)]));
-  for (int64_t i = 0; i < n; ++i) {
-    const int64_t o = ord(i);
-    ords[static_cast<size_t>(remote_rank_[static_cast<size_t>(o)])].push_back(o);
+  std::vector<std::vector<int64_t>> cursor(static_cast<size_t>(nc), std::vector<int64_t>(static_cast<size_t>(P), 0));
+  for (int r = 0; r < P; ++r) {
+    int64_t tot = 0;
+    for (int c = 0; c < nc; ++c) {
+      cursor[static_cast<size_t>(c)][static_cast<size_t>(r)] = tot;
+      tot += ccnt[static_cast<size_t>(c)][static_cast<size_t>(r)];
+    }
+    ords[static_cast<size_t>(r)].resize(static_cast<size_t>(tot));
   }
+  parallel_chunks(n, [&](int c, int64_t b, int64_t e) {
+    auto& cur = cursor[static_cast<size_t>(c)];
+    for (int64_t i = b; i < e; ++i) {
+      const int64_t o = ord(i);
+      const int r = remote_rank_[static_cast<size_t>(o)];
+      ords[static_cast<size_t>(r)][static_cast<size_t>(cur[static_cast<size_t>(r)]++)] = o;
+    }
+  });
   order.clear();
   order.shrink_to_fit();
   pt.mark("order + group by rank");
 
   // Discovery payload: root offsets in edge order (starforest.cpp:96-107).
+  // My own edges do not round-trip through the exchange: the self leaf
+  // group's items are gathered directly below.
+  auto gather_offs = [&](const std::vector<int64_t>& os, int64_t* p) {
+    parallel_chunks(static_cast<int64_t>(os.size()), [&](int, int64_t b, int64_t e) {
+      for (int64_t i = b; i < e; ++i) p[i] = remote_off_[static_cast<size_t>(os[static_cast<size_t>(i)])];
+    });
+  };
   std::vector<std::vector<uint8_t>> send(static_cast<size_t>(P));
   for (int r = 0; r < P; ++r) {
+    if (r == me) continue;
     const auto& os = ords[static_cast<size_t>(r)];
     auto& buf = send[static_cast<size_t>(r)];
     buf.resize(os.size() * sizeof(int64_t));
-    auto* p = reinterpret_cast<int64_t*>(buf.data());
-    for (size_t i = 0; i < os.size(); ++i) p[i] = remote_off_[static_cast<size_t>(os[i])];
+    gather_offs(os, reinterpret_cast<int64_t*>(buf.data()));
   }
+  std::vector<int64_t> self_offs(ords[static_cast<size_t>(me)].size());
+  gather_offs(ords[static_cast<size_t>(me)], self_offs.data());
   pt.mark("payload");
   auto recv = comm_->ctrl().alltoallv(std::move(send));
   pt.mark("discovery exchange");
@@ -205,18 +238,23 @@ void StarForest::setup(SetupAlg alg) {
     roots.push_back(std::move(g));
   }
   for (int r = 0; r < P; ++r) {
-    const auto& b = recv[static_cast<size_t>(r)];
-    if (b.empty()) continue;
-    SFG_REQUIRE(b.size() % sizeof(int64_t) == 0, "malformed setup payload");
     Group g;
     g.rank = r;
-    g.items.resize(b.size() / sizeof(int64_t));
-    std::memcpy(g.items.data(), b.data(), b.size());
-    for (int64_t off : g.items)
-      SFG_REQUIRE(off < nroots_, "setup: leaf on rank " + std::to_string(r) +
-                                     " references root offset " + std::to_string(off) +
-                                     " but this rank has only " + std::to_string(nroots_) +
-                                     " roots");
+    if (r == me) {
+      if (self_offs.empty()) continue;
+      g.items = std::move(self_offs);
+    } else {
+      const auto& b = recv[static_cast<size_t>(r)];
+      if (b.empty()) continue;
+      SFG_REQUIRE(b.size() % sizeof(int64_t) == 0, "malformed setup payload");
+      g.items.resize(b.size() / sizeof(int64_t));
+      std::memcpy(g.items.data(), b.data(), b.size());
+    }
+    const int64_t m = static_cast<int64_t>(g.items.size());
+    const int64_t bad = parallel_find_first(m, [&](int64_t i) { return g.items[static_cast<size_t>(i)] >= nroots_; });
+    SFG_REQUIRE(bad == m, "setup: leaf on rank " + std::to_string(r) + " references root offset " +
+                              std::to_string(bad < m ? g.items[static_cast<size_t>(bad)] : 0) +
+                              " but this rank has only " + std::to_string(nroots_) + " roots");
     leaves.push_back(std::move(g));
   }
   recv.clear();
@@ -230,8 +268,14 @@ void StarForest::setup(SetupAlg alg) {
   self_first_ = !roots.empty() && roots.front().rank == me;
 
   for (auto& g : roots) {
+    if (leaf_local_.empty()) {  // identity: the ordinals are the leaf indices
+      g.pat = Pattern::analyze(g.items.data(), static_cast<int64_t>(g.items.size()));
+      continue;
+    }
     std::vector<int64_t> leaf_idx(g.items.size());
-    for (size_t i = 0; i < g.items.size(); ++i) leaf_idx[i] = leaf_index(g.items[i]);
+    parallel_chunks(static_cast<int64_t>(leaf_idx.size()), [&](int, int64_t b, int64_t e) {
+      for (int64_t i = b; i < e; ++i) leaf_idx[static_cast<size_t>(i)] = leaf_index(g.items[static_cast<size_t>(i)]);
+    });
     g.pat = Pattern::analyze(leaf_idx.data(), static_cast<int64_t>(leaf_idx.size()));
   }
   pt.mark("analyze root groups");
