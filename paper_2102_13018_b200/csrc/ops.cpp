@@ -439,13 +439,15 @@ void end_wait(OpHandle& h, uint64_t tag, const std::vector<XferOp>& recvs) {
 
 // ------------------------------------------------- one-sided (p2p) phases
 //
-// Message counts per directed pair (Staging) replace the reference's
-// SendSig/RecvSig clearing (ops.cpp:160-246): the n-th put from me into d's
-// slot waits in-kernel for d.free[me] >= n-1 and raises d.arrive[me] = n;
-// the unpack of the n-th message from s waits for arrive[s] >= n and its
-// launch raises s.free[me] = n when done. With a small (fused) local part
-// the whole operation is two launches on the caller's stream; a large local
-// scatter runs on the caller's stream while the puts run on the comm stream.
+// Message counts per directed pair and stage region (Staging) replace the
+// reference's SendSig/RecvSig clearing (ops.cpp:160-246): the n-th put from
+// me into region g of d's slot waits in-kernel for free[g][d] >= n-1 and
+// raises d.arrive[g][me] = n; the unpack of the n-th message from s waits
+// for arrive[g][s] >= n and its launch raises s.free[g][me] = n when done.
+// The counters live on the device (advanced by the kernels). Per operation:
+// one put launch on the comm stream (with the local scatter fused in when it
+// is small, otherwise the local scatter runs concurrently on the caller's
+// stream) and one unpack launch.
 bool use_p2p(const OpHandle& h) { return h.sf->comm().p2p() && h.stg && h.stg->flags; }
 
 // The puts always run on the comm stream, so whatever the caller enqueues on
