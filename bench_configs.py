@@ -426,18 +426,23 @@ def config3_spmv(ctx, args):
 
 # ------------------------------------------------------------------ config 3
 def config3(ctx, args):
-    """8 ranks. With 8 GPUs: one process per GPU (NCCL). Otherwise: 8 thread
-    ranks in this process spread over the visible GPUs with the in-process
-    put transport (peer copies), reported as such."""
+    """The ghost-column SF of the 27-point Laplacian. Under torchrun (world
+    > 1): one process per GPU over proc_grid(world) blocks (BASELINE config 3
+    is 8 ranks = 2x2x2; with fewer GPUs the same grid is cut into world
+    blocks), transport --transport, eager and CUDA-graph timings. Single
+    process: 8 thread ranks spread over the visible GPUs with the in-process
+    transport (peer copies), reported as such."""
     import threading
 
     from paper_2102_13018_b200 import graphs
 
     torch, sf = ctx.torch, ctx.sf
     N = args.n3
+    dims = graphs.proc_grid(ctx.world) if ctx.world > 1 else (2, 2, 2)
+    nr = dims[0] * dims[1] * dims[2]
     for permute in (None, 3):
-        specs = [graphs.laplacian27_ghosts(N, (2, 2, 2), r, permute) for r in range(8)]
-        if ctx.world == 8:
+        specs = [graphs.laplacian27_ghosts(N, dims, r, permute) for r in range(nr)]
+        if ctx.world > 1:
             f, setup_s = setup_forest(ctx, specs[ctx.rank])
             u = sf.Unit(sf.Kind.float64)
             root = torch.rand(int(specs[ctx.rank].nroots), dtype=torch.float64, device="cuda")
@@ -452,9 +457,12 @@ def config3(ctx, args):
                 sf.reduce_end(h)
 
             for name, fn in (("bcast_replace", bc), ("reduce_sum", rd)):
-                ms, byts, rec = ctx.timed(fn, args.steps, args.warmup)
-                op_line(ctx, 3, name, ms, byts, rec, {"permuted": permute is not None,
-                                                       "transport": "nccl", "N": N})
+                ms, byts, rec = ctx.timed(fn, args.steps, args.warmup, flush=False)
+                gms = timed_graph(ctx, fn, args.steps, args.warmup)
+                op_line(ctx, 3, name, ms, byts, rec, {"permuted": permute is not None, "N": N,
+                                                       "dims": list(dims), "setup_s": setup_s,
+                                                       "ghosts_rank0": int(specs[0].nleaves),
+                                                       "graph_us_per_op": gms * 1e3})
             continue
         if ctx.rank != 0:
             continue
