@@ -183,7 +183,7 @@ std::vector<TimingRec> timing_collect() {
 
 namespace {
 
-int64_t count_distinct(const std::vector<int64_t>& v, int64_t lo, int64_t hi) {
+int64_t count_distinct(const HostVec<int64_t>& v, int64_t lo, int64_t hi) {
   if (v.size() < 2) return static_cast<int64_t>(v.size());
   const uint64_t span = static_cast<uint64_t>(hi - lo) + 1;
   if (span <= 4 * static_cast<uint64_t>(v.size()) + 4096) {
@@ -196,7 +196,7 @@ int64_t count_distinct(const std::vector<int64_t>& v, int64_t lo, int64_t hi) {
     }
     return d;
   }
-  std::vector<int64_t> sorted(v);
+  std::vector<int64_t> sorted(v.begin(), v.end());
   std::sort(sorted.begin(), sorted.end());
   return static_cast<int64_t>(std::unique(sorted.begin(), sorted.end()) - sorted.begin());
 }
@@ -231,8 +231,7 @@ Pattern Pattern::analyze(const int64_t* idx, int64_t n, bool infer_affine, int64
                          int64_t exy) {
   if (n == 0) return contiguous_range(0, 0);
   const int64_t start = idx[0];
-  int64_t run = 1;
-  while (run < n && idx[run] == start + run) ++run;
+  const int64_t run = parallel_find_first(n, [&](int64_t i) { return idx[i] != start + i; });
   if (run == n) return contiguous_range(start, n);
 
   auto make_affine = [&](int64_t dx, int64_t dy, int64_t dz, int64_t s1, int64_t s2) {

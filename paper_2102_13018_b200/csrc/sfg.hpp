@@ -30,6 +30,30 @@
 
 namespace sfg {
 
+// Host arrays of SetUp size (10^8 edges) are filled right after allocation
+// by parallel loops: an allocator that default-initialises (no zero pass)
+// lets the filling threads take the first-touch page faults in parallel.
+template <class T>
+struct DefaultInit : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = DefaultInit<U>;
+  };
+  DefaultInit() = default;
+  template <class U>
+  DefaultInit(const DefaultInit<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+};
+template <class T>
+using HostVec = std::vector<T, DefaultInit<T>>;
+
 // ---------------------------------------------------------------- vocabulary
 // /root/reference/proj/include/sf/unit.hpp:14-82
 enum class Kind : uint8_t { int32 = 0, int64 = 1, float64 = 2, bytes = 3 };
@@ -126,7 +150,7 @@ struct Pattern {
   int64_t count = 0;
   int64_t start = 0;
   int64_t dx = 0, dy = 0, dz = 0, s1 = 0, s2 = 0;  // affine
-  std::vector<int64_t> idx;                         // indexed
+  HostVec<int64_t> idx;                             // indexed
   bool has_duplicates = false;
   int64_t distinct = 0;  // number of distinct indices
   int64_t bound = 0;  // largest index + 1 (0 when empty)
@@ -277,7 +301,7 @@ enum class SetupAlg { automatic = 0, dense = 1, consensus = 2 };
 // One neighbor group, aligned across the pair (starforest.hpp:47-55,110-121).
 struct Group {
   int rank = -1;
-  std::vector<int64_t> items;  // root groups: leaf ordinals; leaf groups: root offsets
+  HostVec<int64_t> items;  // root groups: leaf ordinals; leaf groups: root offsets
   Pattern pat;                 // root groups: leaf-index pattern; leaf groups: root pattern
 };
 
@@ -435,9 +459,9 @@ class StarForest {
   int64_t nroots_ = 0, nleaves_ = 0, leaf_bound_ = 0;
   bool contiguous_leaves_ = true;
   bool has_local_ = false;
-  std::vector<int64_t> leaf_local_;
-  std::vector<int32_t> remote_rank_;
-  std::vector<int64_t> remote_off_;
+  HostVec<int64_t> leaf_local_;
+  HostVec<int32_t> remote_rank_;
+  HostVec<int64_t> remote_off_;
   std::vector<Group> root_groups_, leaf_groups_;
   bool self_first_ = false;
   std::unique_ptr<StarForest> multi_;

@@ -184,7 +184,7 @@ void StarForest::setup(SetupAlg alg) {
     auto& k = ccnt[static_cast<size_t>(c)];
     for (int64_t i = b; i < e; ++i) ++k[static_cast<size_t>(remote_rank_[static_cast<size_t>(ord(i))])];
   });
-  std::vector<std::vector<int64_t>> ords(static_cast<size_t>(P));
+  std::vector<HostVec<int64_t>> ords(static_cast<size_t>(P));
   std::vector<std::vector<int64_t>> cursor(static_cast<size_t>(nc), std::vector<int64_t>(static_cast<size_t>(P), 0));
   for (int r = 0; r < P; ++r) {
     int64_t tot = 0;
@@ -209,7 +209,7 @@ void StarForest::setup(SetupAlg alg) {
   // Discovery payload: root offsets in edge order (starforest.cpp:96-107).
   // My own edges do not round-trip through the exchange: the self leaf
   // group's items are gathered directly below.
-  auto gather_offs = [&](const std::vector<int64_t>& os, int64_t* p) {
+  auto gather_offs = [&](const HostVec<int64_t>& os, int64_t* p) {
     parallel_chunks(static_cast<int64_t>(os.size()), [&](int, int64_t b, int64_t e) {
       for (int64_t i = b; i < e; ++i) p[i] = remote_off_[static_cast<size_t>(os[static_cast<size_t>(i)])];
     });
@@ -222,7 +222,7 @@ void StarForest::setup(SetupAlg alg) {
     buf.resize(os.size() * sizeof(int64_t));
     gather_offs(os, reinterpret_cast<int64_t*>(buf.data()));
   }
-  std::vector<int64_t> self_offs(ords[static_cast<size_t>(me)].size());
+  HostVec<int64_t> self_offs(ords[static_cast<size_t>(me)].size());
   gather_offs(ords[static_cast<size_t>(me)], self_offs.data());
   pt.mark("payload");
   auto recv = comm_->ctrl().alltoallv(std::move(send));
@@ -272,7 +272,7 @@ void StarForest::setup(SetupAlg alg) {
       g.pat = Pattern::analyze(g.items.data(), static_cast<int64_t>(g.items.size()));
       continue;
     }
-    std::vector<int64_t> leaf_idx(g.items.size());
+    HostVec<int64_t> leaf_idx(g.items.size());
     parallel_chunks(static_cast<int64_t>(leaf_idx.size()), [&](int, int64_t b, int64_t e) {
       for (int64_t i = b; i < e; ++i) leaf_idx[static_cast<size_t>(i)] = leaf_index(g.items[static_cast<size_t>(i)]);
     });
