@@ -106,6 +106,37 @@ def main():
                         except AssertionError as e:
                             fails.append(f"graph {e}")
                 del g
+                # FetchAndOp SUM in a graph: every replay serialises the same
+                # contributions again on top of the previous roots.
+                ri0 = dev(iroots[rank])
+                li0 = dev(ileaves[rank])
+                up = torch.zeros_like(li0)
+                with torch.cuda.stream(st):
+                    sf.fetch_and_op_end(sf.fetch_and_op_begin(f, ui, ri0, li0, up, sf.ReduceOp.sum, st))
+                torch.cuda.synchronize()
+                ri0.copy_(dev(iroots[rank]))
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st):
+                    sf.fetch_and_op_end(sf.fetch_and_op_begin(f, ui, ri0, li0, up, sf.ReduceOp.sum, st))
+                cur = [x.copy() for x in iroots]
+                for it in range(2):
+                    g.replay()
+                    torch.cuda.synchronize()
+                    got = [ri0.cpu().numpy(), up.cpu().numpy()]
+                    allg = [None] * world
+                    dist.all_gather_object(allg, got)
+                    if rank == 0:
+                        try:
+                            orr, ou = O.fetch_and_op(specs, cur, ileaves, [np.zeros_like(x) for x in ileaves], "sum")
+                            assert_same([a[0] for a in allg], orr, what=f"{name} graph fetch root {it}")
+                            assert_same([a[1] for a in allg], ou, what=f"{name} graph fetch update {it}")
+                        except AssertionError as e:
+                            fails.append(f"graph {e}")
+                    cur = orr if rank == 0 else cur
+                    obj = [cur]
+                    dist.broadcast_object_list(obj, src=0)
+                    cur = obj[0]
+                del g
             del f
         comm.close()
     dist.barrier()
