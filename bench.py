@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--sample-steps", type=int, default=10)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--dims", type=lambda v: tuple(int(x) for x in v.split(",")), default=None,
+                   help="process grid px,py,pz (default: 1x1x2 / 1x2x2 / 2x2x2 for 2 / 4 / 8 GPUs)")
     p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                    help="remote exchange at N>1: one-sided NVLink puts (p2p) or grouped NCCL send/recv")
     return p.parse_args()
@@ -214,8 +216,8 @@ def halo_exchange(args, sf, comm, graphs, torch, rank, world, allreduce, barrier
     faces, no interior self edges), Bcast REPLACE captured 20x in a CUDA
     graph and replayed (device time; no Python launch overhead). achieved =
     bytes this GPU sends per exchange / time per exchange, slowest rank."""
-    spec = graphs.g2l_halo(args.N, world, rank, interior=False)
-    geo = graphs.G2L(args.N, world, rank)
+    spec = graphs.g2l_halo(args.N, world, rank, dims=args.dims, interior=False)
+    geo = graphs.G2L(args.N, world, rank, dims=args.dims)
     f = sf.StarForest(comm)
     f.set_graph_spec(spec)
     f.setup()
@@ -294,8 +296,8 @@ def ours(args, rank, world, local):
         return float(t.item())
 
     t0 = time.perf_counter()
-    spec = graphs.g2l_halo(args.N, world, rank)
-    geo = graphs.G2L(args.N, world, rank)
+    spec = graphs.g2l_halo(args.N, world, rank, dims=args.dims)
+    geo = graphs.G2L(args.N, world, rank, dims=args.dims)
     gen_s = time.perf_counter() - t0
     f = sf.StarForest(comm)
     f.set_graph_spec(spec)
@@ -449,7 +451,7 @@ def ours(args, rank, world, local):
             cpu = {"value": None, "error": str(e)}
 
     if rank == 0:
-        px, py, pz = graphs.proc_grid(world)
+        px, py, pz = args.dims or graphs.proc_grid(world)
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
