@@ -146,7 +146,6 @@ struct LaunchParams {
   int64_t bl = 1;  // elements per vertex
   FastDiv bldiv;
   int nseg = 0;
-  int vec_ok = 0;  // reserved
   // p2p: flags segments wait on (bit i of DSeg::wait_mask = waits[i]) and the
   // acknowledgements the launch raises once all its CTAs are done (advance
   // the local counter *done_seq[i], publish it in a peer's "slot free" flag

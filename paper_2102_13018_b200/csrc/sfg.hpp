@@ -535,7 +535,6 @@ struct DevMatrix {
   struct Sell {
     int64_t rows = 0, cols = 0, nnz = 0, slots = 0;
     int64_t* slice_off = nullptr;
-    int32_t* slice_w = nullptr;
     int32_t* row_len = nullptr;
     int32_t* col = nullptr;
     void* val = nullptr;

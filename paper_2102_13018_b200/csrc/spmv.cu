@@ -42,7 +42,6 @@ __device__ __forceinline__ T add_rn(T a, T b) {
 // y[r] (=|+=) sum_k vals * x[col], k in the row's CSR order.
 template <class T, bool ADD, bool PLUS_ZERO>
 __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t rows, const int64_t* __restrict__ slice_off,
-                                                        const int32_t* __restrict__ slice_w,
                                                         const int32_t* __restrict__ row_len,
                                                         const int32_t* __restrict__ col,
                                                         const T* __restrict__ val, const T* __restrict__ x,
@@ -72,7 +71,6 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t rows, const int6
     const int64_t e = base + static_cast<int64_t>(k) * 32;
     acc = add_rn(acc, mul_rn(__ldg(val + e), __ldg(x + __ldg(col + e))));
   }
-  (void)slice_w;
   if constexpr (PLUS_ZERO) acc = add_rn(acc, T(0));
   y[r] = ADD ? add_rn(y[r], acc) : acc;
 }
@@ -81,7 +79,7 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t rows, const int6
 // a slice; padding slots are never read).
 struct SellHost {
   std::vector<int64_t> slice_off;
-  std::vector<int32_t> slice_w, row_len, col;
+  std::vector<int32_t> row_len, col;
   std::vector<uint8_t> val;  // elem-size bytes per slot
 };
 
@@ -90,7 +88,6 @@ SellHost to_sell(int64_t rows, const int64_t* rowptr, const int64_t* colind, con
   SellHost h;
   const int64_t nslices = (rows + 31) / 32;
   h.slice_off.resize(static_cast<size_t>(nslices) + 1);
-  h.slice_w.resize(static_cast<size_t>(nslices));
   h.row_len.resize(static_cast<size_t>(rows));
   int64_t off = 0;
   for (int64_t s = 0; s < nslices; ++s) {
@@ -102,7 +99,6 @@ SellHost to_sell(int64_t rows, const int64_t* rowptr, const int64_t* colind, con
       w = std::max(w, static_cast<int32_t>(len));
     }
     h.slice_off[static_cast<size_t>(s)] = off;
-    h.slice_w[static_cast<size_t>(s)] = w;
     off += static_cast<int64_t>(w) * 32;
   }
   h.slice_off[static_cast<size_t>(nslices)] = off;
@@ -150,7 +146,6 @@ void upload_sell(const SellHost& h, size_t esz, DevMatrix::Sell& d, std::vector<
   };
   d.rows = static_cast<int64_t>(h.row_len.size());
   d.slice_off = static_cast<int64_t*>(up(h.slice_off.data(), h.slice_off.size() * sizeof(int64_t)));
-  d.slice_w = static_cast<int32_t*>(up(h.slice_w.data(), h.slice_w.size() * sizeof(int32_t)));
   d.row_len = static_cast<int32_t*>(up(h.row_len.data(), h.row_len.size() * sizeof(int32_t)));
   d.col = static_cast<int32_t*>(up(h.col.data(), h.col.size() * sizeof(int32_t)));
   d.val = up(h.val.data(), h.val.size());
@@ -169,7 +164,7 @@ void launch_sell(const DevMatrix::Sell& m, const void* x, void* y, cudaStream_t 
     e1 = timing_event();
     SFG_CUDA(cudaEventRecord(e0, s));
   }
-  sell_spmv_kernel<T, ADD, PLUS_ZERO><<<blocks, 256, 0, s>>>(m.rows, m.slice_off, m.slice_w, m.row_len, m.col,
+  sell_spmv_kernel<T, ADD, PLUS_ZERO><<<blocks, 256, 0, s>>>(m.rows, m.slice_off, m.row_len, m.col,
                                                   static_cast<const T*>(m.val), static_cast<const T*>(x),
                                                   static_cast<T*>(y));
   SFG_CUDA(cudaGetLastError());
