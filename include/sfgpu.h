@@ -134,6 +134,12 @@ int sfg_sf_destroy(sfg_sf sf);
  * the RootRef{rank, offset} list split in two arrays. Host pointers. */
 int sfg_sf_set_graph(sfg_sf sf, int64_t nroots, int64_t nleaves, const int64_t* leaf_local,
                      const int32_t* remote_rank, const int64_t* remote_off);
+/* set_graph with the three arrays in the communicator's DEVICE memory (the
+ * graph already lives in HBM): same contract, validation and
+ * messages as sfg_sf_set_graph; sfg_sf_setup then plans on the GPU
+ * (group lists stay in HBM, host copies are made only when asked for). */
+int sfg_sf_set_graph_device(sfg_sf sf, int64_t nroots, int64_t nleaves, const int64_t* leaf_local,
+                            const int32_t* remote_rank, const int64_t* remote_off);
 /* StarForest::setup (starforest.hpp:79; starforest.cpp:82-161). Collective. */
 int sfg_sf_setup(sfg_sf sf, int alg);
 int sfg_sf_get_info(sfg_sf sf, sfg_sf_info* out);

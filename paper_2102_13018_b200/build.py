@@ -72,7 +72,7 @@ def build(verbose: bool = False) -> str:
     cuda = _cuda_home()
     nvcc = os.path.join(cuda, "bin", "nvcc")
     headers = sorted(glob.glob(os.path.join(CSRC, "*.hpp"))) + [os.path.join(INCLUDE, "sfgpu.h")]
-    cu_flags = [nvcc, "-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC",
+    cu_flags = [nvcc, "-std=c++17", "-O3", "-lineinfo", "--extended-lambda", *ARCH, "-Xcompiler", "-fPIC",
                 "-Xptxas", "-v" if verbose else "-O3", f"-I{CSRC}", f"-I{INCLUDE}"]
     cxx_flags = ["g++", "-std=c++17", "-O2", "-g", "-fPIC", "-Wall", "-Wextra",
                  "-Wno-unused-parameter", f"-I{cuda}/include", f"-I{CSRC}", f"-I{INCLUDE}"]

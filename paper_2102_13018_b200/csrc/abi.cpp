@@ -278,6 +278,11 @@ int sfg_sf_set_graph(sfg_sf sf, int64_t nroots, int64_t nleaves, const int64_t* 
   return guard([&] { SF(sf)->set_graph(nroots, nleaves, leaf_local, remote_rank, remote_off); });
 }
 
+int sfg_sf_set_graph_device(sfg_sf sf, int64_t nroots, int64_t nleaves, const int64_t* leaf_local,
+                            const int32_t* remote_rank, const int64_t* remote_off) {
+  return guard([&] { SF(sf)->set_graph_device(nroots, nleaves, leaf_local, remote_rank, remote_off); });
+}
+
 int sfg_sf_setup(sfg_sf sf, int alg) {
   return guard([&] { SF(sf)->setup(static_cast<sfg::SetupAlg>(alg)); });
 }
@@ -307,13 +312,14 @@ int sfg_sf_group(sfg_sf sf, int which, int g, int* rank, int64_t* nitems, sfg_pa
     const auto& gs = which == 0 ? SF(sf)->root_groups() : SF(sf)->leaf_groups();
     SFG_REQUIRE(g >= 0 && g < static_cast<int>(gs.size()), "group index out of range");
     if (rank) *rank = gs[static_cast<size_t>(g)].rank;
-    if (nitems) *nitems = static_cast<int64_t>(gs[static_cast<size_t>(g)].items.size());
+    if (nitems) *nitems = gs[static_cast<size_t>(g)].count();
     if (pat) fill_pattern(gs[static_cast<size_t>(g)].pat, pat);
   });
 }
 
 int sfg_sf_group_items(sfg_sf sf, int which, int g, int64_t* items) {
   return guard([&] {
+    SF(sf)->host_graph();
     const auto& gs = which == 0 ? SF(sf)->root_groups() : SF(sf)->leaf_groups();
     SFG_REQUIRE(g >= 0 && g < static_cast<int>(gs.size()), "group index out of range");
     const auto& v = gs[static_cast<size_t>(g)].items;
@@ -335,6 +341,7 @@ int sfg_sf_multi_sf(sfg_sf sf, sfg_sf* out) {
 int sfg_sf_graph(sfg_sf sf, int64_t* leaf_index, int32_t* remote_rank, int64_t* remote_off) {
   return guard([&] {
     auto* s = SF(sf);
+    s->host_graph();
     for (int64_t o = 0; o < s->nleaves(); ++o) {
       if (leaf_index) leaf_index[o] = s->leaf_index(o);
       if (remote_rank) remote_rank[o] = s->remote_rank_of(o);

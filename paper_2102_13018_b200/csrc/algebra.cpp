@@ -78,7 +78,9 @@ std::unique_ptr<StarForest> build(Comm& c, int64_t nroots, std::vector<std::arra
 // edge where an A leaf and a B root coincide on (rank, index).
 std::unique_ptr<StarForest> compose(StarForest& A, StarForest& B) {
   A.require_state(SfState::set_up, "compose");
+  A.host_graph();
   B.require_state(SfState::set_up, "compose");
+  B.host_graph();
   same_comm(A, B, "compose");
   Comm& c = A.comm();
   const int P = c.size();
@@ -122,7 +124,9 @@ std::unique_ptr<StarForest> compose(StarForest& A, StarForest& B) {
 // starforest.hpp:156-159: roots of AB are A's roots, leaves are B's roots.
 std::unique_ptr<StarForest> compose_inverse(StarForest& A, StarForest& B) {
   A.require_state(SfState::set_up, "compose_inverse");
+  A.host_graph();
   B.require_state(SfState::set_up, "compose_inverse");
+  B.host_graph();
   same_comm(A, B, "compose_inverse");
   Comm& c = A.comm();
   const int P = c.size();
@@ -168,6 +172,7 @@ std::unique_ptr<StarForest> compose_inverse(StarForest& A, StarForest& B) {
 // starforest.hpp:161-167: keep the edges whose root is selected.
 std::unique_ptr<StarForest> embed_root(StarForest& f, const int64_t* sel, int64_t nsel) {
   f.require_state(SfState::set_up, "embed_root");
+  f.host_graph();
   Comm& c = f.comm();
   const int P = c.size();
   std::vector<uint8_t> flag(static_cast<size_t>(f.nroots()), 0);
@@ -207,6 +212,7 @@ std::unique_ptr<StarForest> embed_root(StarForest& f, const int64_t* sel, int64_
 // starforest.hpp:161-167: keep the edges whose leaf index is selected.
 std::unique_ptr<StarForest> embed_leaf(StarForest& f, const int64_t* sel, int64_t nsel) {
   f.require_state(SfState::set_up, "embed_leaf");
+  f.host_graph();
   std::vector<int64_t> s(sel, sel + nsel);
   for (int64_t l : s) SFG_REQUIRE(l >= 0, "embed_leaf: selected leaf index is negative");
   std::sort(s.begin(), s.end());

@@ -1,0 +1,642 @@
+// Device-side SetGraph + SetUp: the planner of
+// starforest.cpp run on the GPU for graphs that already live in HBM.
+//
+// Reference: /root/reference/proj/src/starforest.cpp:29-161 (the same
+// contract and error messages as the host planner), pattern.cpp:13-64 for the
+// classification. The host planner (starforest.cpp StarForest::setup,
+// pattern.cpp Pattern::analyze) is the specification; this file reproduces
+// its results — group ranks, items, order and patterns — with:
+//   validation / order checks   one pass, first offending position by atomicMin
+//   leaf-index order            CUB stable radix sort of (leaf index, ordinal)
+//                               only when the indices are not increasing
+//   grouping by root rank       CUB stable radix sort on ceil(log2 P) key bits
+//   discovery payload           gather off[ords]; the self segment never
+//                               leaves HBM, remote segments cross the control
+//                               plane (halo-sized for partitioned grids)
+//   pattern classification      device find-first passes for contiguity and
+//                               the Affine3D inference + full verification;
+//                               distinct counts by bitmap or sorted uniques
+// Everything is synchronous on cudaStreamPerThread (SetUp is collective and
+// blocking in the reference too). Group items stay in HBM; host copies are
+// made on demand by host_graph() for host-side consumers.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "sfg.hpp"
+
+namespace sfg {
+
+namespace {
+
+constexpr int kT = 256;
+constexpr int64_t kI32Max = (int64_t(1) << 31) - 1;
+using u64 = unsigned long long;
+
+cudaStream_t dstream() { return cudaStreamPerThread; }
+
+int grid_for(int64_t n) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (n + kT - 1) / kT;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(sms) * 8)));
+}
+
+template <class T>
+T* dalloc(int64_t n) {
+  void* p = nullptr;
+  if (n > 0) SFG_CUDA(cudaMalloc(&p, static_cast<size_t>(n) * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+template <class T>
+T read1(const T* d) {
+  T v{};
+  SFG_CUDA(cudaMemcpyAsync(&v, d, sizeof(T), cudaMemcpyDeviceToHost, dstream()));
+  SFG_CUDA(cudaStreamSynchronize(dstream()));
+  return v;
+}
+
+__device__ __forceinline__ u64 warp_min(u64 v) {
+  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide min of one value per thread into *out (atomicMin).
+__device__ __forceinline__ void block_min_to(u64 v, u64* out) {
+  __shared__ u64 red[kT / 32];
+  v = warp_min(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    u64 w = threadIdx.x < kT / 32 ? red[threadIdx.x] : ~0ull;
+    w = warp_min(w);
+    if (threadIdx.x == 0 && w != ~0ull) atomicMin(out, w);
+  }
+  __syncthreads();
+}
+
+__global__ void k_fill(u64* p, int k, u64 v) {
+  if (static_cast<int>(threadIdx.x) < k) p[threadIdx.x] = v;
+}
+
+// First position at which pred(i) holds, or n: grid-stride, per-thread
+// first hit, block min, one atomicMin per block.
+template <class Pred>
+__global__ void __launch_bounds__(kT) k_find_first(int64_t n, Pred pred, u64* out) {
+  u64 first = ~0ull;
+  for (int64_t i = blockIdx.x * int64_t(kT) + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT)
+    if (pred(i)) {
+      first = static_cast<u64>(i);
+      break;
+    }
+  block_min_to(first, out);
+}
+
+// Scratch for find-first results (one per forest call site, small).
+struct Scratch {
+  u64* v = nullptr;
+  Scratch() { SFG_CUDA(cudaMalloc(&v, 8 * sizeof(u64))); }
+  ~Scratch() { cudaFree(v); }
+};
+
+template <class Pred>
+int64_t find_first(int64_t n, Pred pred, Scratch& sc) {
+  if (n <= 0) return n;
+  k_fill<<<1, 32, 0, dstream()>>>(sc.v, 1, static_cast<u64>(n));
+  k_find_first<<<grid_for(n), kT, 0, dstream()>>>(n, pred, sc.v);
+  SFG_CUDA(cudaGetLastError());
+  const u64 r = read1(sc.v);
+  return static_cast<int64_t>(std::min<u64>(r, static_cast<u64>(n)));
+}
+
+__global__ void k_iota(int64_t* p, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(kT) + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT) p[i] = i;
+}
+
+template <class T>
+__global__ void k_gather(const T* __restrict__ src, const int64_t* __restrict__ idx, T* __restrict__ dst,
+                         int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(kT) + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT)
+    dst[i] = src[idx[i]];
+}
+
+// first[k] = first position of key k in the sorted keys (untouched if absent).
+__global__ void k_key_starts(const int32_t* keys, int64_t n, int64_t* first) {
+  for (int64_t i = blockIdx.x * int64_t(kT) + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT)
+    if (i == 0 || keys[i] != keys[i - 1]) first[keys[i]] = i;
+}
+
+__global__ void k_minmax(const int64_t* idx, int64_t n, long long* mm) {
+  long long lo = LLONG_MAX, hi = LLONG_MIN;
+  for (int64_t i = blockIdx.x * int64_t(kT) + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT) {
+    lo = min(lo, static_cast<long long>(idx[i]));
+    hi = max(hi, static_cast<long long>(idx[i]));
+  }
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&mm[0], lo);
+    atomicMax(&mm[1], hi);
+  }
+}
+
+// Distinct values by bitmap over [lo, lo + 32*words): count bits newly set.
+__global__ void k_bitmap_distinct(const int64_t* idx, int64_t n, int64_t lo, uint32_t* bits, u64* count,
+                                  u64* repeat) {
+  u64 fresh = 0, rep = 0;
+  for (int64_t i = blockIdx.x * int64_t(kT) + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT) {
+    const uint64_t x = static_cast<uint64_t>(idx[i] - lo);
+    const uint32_t b = 1u << (x & 31);
+    const uint32_t old = atomicOr(&bits[x >> 5], b);
+    if (old & b)
+      rep = 1;
+    else
+      ++fresh;
+  }
+  for (int o = 16; o; o >>= 1) {
+    fresh += __shfl_xor_sync(0xffffffffu, fresh, o);
+    rep |= __shfl_xor_sync(0xffffffffu, rep, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (count && fresh) atomicAdd(count, fresh);
+    if (repeat && rep) atomicOr(repeat, rep);
+  }
+}
+
+__global__ void k_count_uniques(const int64_t* sorted, int64_t n, u64* count) {
+  u64 c = 0;
+  for (int64_t i = blockIdx.x * int64_t(kT) + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT)
+    c += (i == 0 || sorted[i] != sorted[i - 1]);
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+__global__ void k_narrow(const int64_t* src, int64_t n, int32_t* dst, u64* bad) {
+  u64 first = ~0ull;
+  for (int64_t i = blockIdx.x * int64_t(kT) + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT) {
+    const int64_t v = src[i];
+    if (v > kI32Max && first == ~0ull) first = static_cast<u64>(i);
+    dst[i] = static_cast<int32_t>(v);
+  }
+  block_min_to(first, bad);
+}
+
+// CUB radix sort of (key, value) pairs, stable, on bits [0, end_bit).
+template <class K, class V>
+void sort_pairs(const K* kin, K* kout, const V* vin, V* vout, int64_t n, int end_bit) {
+  size_t tmp = 0;
+  SFG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, n, 0, end_bit, dstream()));
+  void* t = nullptr;
+  SFG_CUDA(cudaMallocAsync(&t, tmp, dstream()));
+  SFG_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, kin, kout, vin, vout, n, 0, end_bit, dstream()));
+  SFG_CUDA(cudaFreeAsync(t, dstream()));
+}
+
+template <class K>
+void sort_keys(const K* kin, K* kout, int64_t n) {
+  size_t tmp = 0;
+  SFG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, kin, kout, n, 0, int(sizeof(K) * 8), dstream()));
+  void* t = nullptr;
+  SFG_CUDA(cudaMallocAsync(&t, tmp, dstream()));
+  SFG_CUDA(cub::DeviceRadixSort::SortKeys(t, tmp, kin, kout, n, 0, int(sizeof(K) * 8), dstream()));
+  SFG_CUDA(cudaFreeAsync(t, dstream()));
+}
+
+int64_t count_distinct_dev(const int64_t* idx, int64_t n, int64_t lo, int64_t hi, Scratch& sc) {
+  if (n < 2) return n;
+  const uint64_t span = static_cast<uint64_t>(hi - lo) + 1;
+  k_fill<<<1, 32, 0, dstream()>>>(sc.v, 1, 0);
+  if (span <= 4 * static_cast<uint64_t>(n) + 4096) {
+    const int64_t words = static_cast<int64_t>((span + 31) / 32);
+    uint32_t* bits = nullptr;
+    SFG_CUDA(cudaMallocAsync(&bits, static_cast<size_t>(words) * 4, dstream()));
+    SFG_CUDA(cudaMemsetAsync(bits, 0, static_cast<size_t>(words) * 4, dstream()));
+    k_bitmap_distinct<<<grid_for(n), kT, 0, dstream()>>>(idx, n, lo, bits, sc.v, nullptr);
+    SFG_CUDA(cudaFreeAsync(bits, dstream()));
+  } else {
+    int64_t* sorted = nullptr;
+    SFG_CUDA(cudaMallocAsync(&sorted, static_cast<size_t>(n) * 8, dstream()));
+    sort_keys(idx, sorted, n);
+    k_count_uniques<<<grid_for(n), kT, 0, dstream()>>>(sorted, n, sc.v);
+    SFG_CUDA(cudaFreeAsync(sorted, dstream()));
+  }
+  SFG_CUDA(cudaGetLastError());
+  return static_cast<int64_t>(read1(sc.v));
+}
+
+// Pattern::analyze (pattern.cpp:230-299, infer_affine, no extents) over a
+// list in HBM; indexed patterns keep the list there (Pattern::didx).
+Pattern analyze_dev(const int64_t* idx, int64_t n, Scratch& sc) {
+  if (n == 0) return Pattern::contiguous_range(0, 0);
+  const int64_t start = read1(idx);
+  const int64_t run = find_first(n, [=] __device__(int64_t i) { return idx[i] != start + i; }, sc);
+  if (run == n) return Pattern::contiguous_range(start, n);
+
+  if (start >= 0) {
+    const int64_t dx = run;
+    if (n % dx == 0) {
+      const int64_t rows = n / dx;
+      const int64_t s1 = read1(idx + dx) - start;
+      if (s1 >= dx) {
+        // dy = first row r >= 1 not at start + r*s1 (capped at rows)
+        const int64_t dy = 1 + find_first(
+                                   rows - 1,
+                                   [=] __device__(int64_t r) {
+                                     return idx[(r + 1) * dx] != start + (r + 1) * s1;
+                                   },
+                                   sc);
+        if (rows % dy == 0) {
+          const int64_t dz = rows / dy;
+          const int64_t s2 = dz > 1 ? read1(idx + dy * dx) - start : dy * s1;
+          const bool planes_ok = dz == 1 || s2 >= (dy - 1) * s1 + dx;
+          if (planes_ok && dx < (int64_t(1) << 31) && dy < (int64_t(1) << 31)) {
+            const int64_t plane = dx * dy;
+            const int64_t bad = find_first(
+                n,
+                [=] __device__(int64_t i) {
+                  const int64_t r = i / dx, x = i - r * dx;
+                  const int64_t k = i / plane, j = r - k * dy;
+                  return idx[i] != start + k * s2 + j * s1 + x;
+                },
+                sc);
+            if (bad == n) {
+              Pattern p;
+              p.kind = Pattern::affine;
+              p.count = n;
+              p.start = start;
+              p.dx = dx;
+              p.dy = dy;
+              p.dz = dz;
+              p.s1 = s1;
+              p.s2 = s2;
+              p.bound = start + (dz - 1) * s2 + (dy - 1) * s1 + dx;
+              p.distinct = n;
+              return p;
+            }
+          }
+        }
+      }
+    }
+  }
+
+  Pattern p;
+  p.kind = Pattern::indexed;
+  p.count = n;
+  p.didx = idx;
+  long long* mm = reinterpret_cast<long long*>(sc.v + 2);
+  const long long init[2] = {LLONG_MAX, LLONG_MIN};
+  SFG_CUDA(cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, dstream()));
+  k_minmax<<<grid_for(n), kT, 0, dstream()>>>(idx, n, mm);
+  SFG_CUDA(cudaGetLastError());
+  long long got[2];
+  SFG_CUDA(cudaMemcpyAsync(got, mm, sizeof(got), cudaMemcpyDeviceToHost, dstream()));
+  SFG_CUDA(cudaStreamSynchronize(dstream()));
+  p.start = got[0];
+  p.bound = got[1] + 1;
+  p.distinct = count_distinct_dev(idx, n, got[0], got[1], sc);
+  p.has_duplicates = p.distinct < n;
+  return p;
+}
+
+}  // namespace
+
+DevGraph::~DevGraph() {
+  if (device >= 0) cudaSetDevice(device);
+  cudaDeviceSynchronize();
+  int64_t* bufs[] = {local, off, ords, ridx != ords && ridx != local ? ridx : nullptr, loffs};
+  for (int64_t* b : bufs)
+    if (b) cudaFree(b);
+  if (rank) cudaFree(rank);
+}
+
+void dev_narrow_index(const int64_t* src, int64_t n, int32_t* dst) {
+  if (n <= 0) return;
+  Scratch sc;
+  k_fill<<<1, 32, 0, dstream()>>>(sc.v, 1, ~0ull);
+  k_narrow<<<grid_for(n), kT, 0, dstream()>>>(src, n, dst, sc.v);
+  SFG_CUDA(cudaGetLastError());
+  SFG_REQUIRE(read1(sc.v) == ~0ull, "index exceeds the int32 range of device plans");
+}
+
+bool dev_any_repeat(const std::vector<std::pair<const int64_t*, int64_t>>& lists, int64_t bound) {
+  if (bound <= 0) return false;
+  Scratch sc;
+  const int64_t words = (bound + 31) / 32;
+  uint32_t* bits = dalloc<uint32_t>(words);
+  SFG_CUDA(cudaMemsetAsync(bits, 0, static_cast<size_t>(words) * 4, dstream()));
+  k_fill<<<1, 32, 0, dstream()>>>(sc.v, 1, 0);
+  for (const auto& [p, n] : lists)
+    if (n > 0) k_bitmap_distinct<<<grid_for(n), kT, 0, dstream()>>>(p, n, 0, bits, nullptr, sc.v);
+  SFG_CUDA(cudaGetLastError());
+  const bool rep = read1(sc.v) != 0;
+  SFG_CUDA(cudaFree(bits));
+  return rep;
+}
+
+// set_graph (starforest.cpp:29-76) with the arrays in device memory: the
+// same validation order and messages as StarForest::set_graph.
+void StarForest::set_graph_device(int64_t nroots, int64_t nleaves, const int64_t* leaf_local,
+                                  const int32_t* remote_rank, const int64_t* remote_off) {
+  SFG_REQUIRE(state_ == SfState::created || state_ == SfState::graph_set,
+              "set_graph requires a created or graph-set star forest");
+  SFG_REQUIRE(nroots >= 0 && nleaves >= 0, "set_graph: negative root or leaf count");
+  SFG_REQUIRE(nleaves == 0 || (remote_rank != nullptr && remote_off != nullptr),
+              "set_graph: leaf_remote length does not match nleaves");
+  SFG_REQUIRE(comm_->has_device(), "set_graph_device needs a communicator with a device");
+  comm_->bind_device();
+  const int64_t n = nleaves;
+  Scratch sc;
+  auto g = std::make_unique<DevGraph>();
+  g->device = comm_->device();
+
+  int64_t bound = n;
+  bool contiguous = true;
+  if (leaf_local != nullptr && n > 0) {
+    const int64_t* L = leaf_local;
+    const bool increasing =
+        find_first(n, [=] __device__(int64_t i) { return i > 0 && L[i] <= L[i - 1]; }, sc) == n;
+    contiguous = find_first(n, [=] __device__(int64_t i) { return L[i] != i; }, sc) == n;
+    g->ascending = increasing;
+    if (increasing) {
+      SFG_REQUIRE(read1(L) >= 0, "set_graph: negative leaf index");
+      bound = read1(L + n - 1) + 1;
+    } else {
+      int64_t* sorted = dalloc<int64_t>(n);
+      sort_keys(L, sorted, n);
+      const int64_t lo = read1(sorted);
+      if (lo < 0) {
+        cudaFree(sorted);
+        fail("set_graph: negative leaf index");
+      }
+      const int64_t dup = find_first(n, [=] __device__(int64_t i) { return i > 0 && sorted[i] == sorted[i - 1]; }, sc);
+      if (dup < n) {
+        const int64_t v = read1(sorted + dup);
+        cudaFree(sorted);
+        fail("set_graph: duplicate leaf index " + std::to_string(v) + " violates the forest property");
+      }
+      bound = read1(sorted + n - 1) + 1;
+      SFG_CUDA(cudaFree(sorted));
+    }
+  } else if (leaf_local != nullptr) {
+    bound = 0;
+  }
+  const int nranks = comm_->size();
+  const int32_t* R = remote_rank;
+  const int64_t* O = remote_off;
+  const int64_t bad = find_first(
+      n, [=] __device__(int64_t i) { return R[i] < 0 || R[i] >= nranks || O[i] < 0; }, sc);
+  if (bad < n) {
+    const int32_t r = read1(R + bad);
+    SFG_REQUIRE(r >= 0 && r < nranks, "set_graph: root rank " + std::to_string(r) + " outside communicator");
+    fail("set_graph: negative root offset");
+  }
+
+  // Own copies, like the host set_graph (the caller may free its arrays).
+  auto copy = [&](auto*& dst, const auto* src) {
+    using T = std::remove_const_t<std::remove_pointer_t<decltype(src)>>;
+    dst = dalloc<T>(n);
+    if (n) SFG_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(n) * sizeof(T), cudaMemcpyDeviceToDevice, dstream()));
+  };
+  if (leaf_local != nullptr && !contiguous) copy(g->local, leaf_local);
+  copy(g->rank, remote_rank);
+  copy(g->off, remote_off);
+  SFG_CUDA(cudaStreamSynchronize(dstream()));
+
+  nroots_ = nroots;
+  nleaves_ = nleaves;
+  leaf_bound_ = bound;
+  contiguous_leaves_ = contiguous;
+  has_local_ = leaf_local != nullptr;
+  leaf_local_.clear();
+  remote_rank_.clear();
+  remote_off_.clear();
+  root_groups_.clear();
+  leaf_groups_.clear();
+  self_first_ = false;
+  multi_.reset();
+  dev_.reset();
+  staging_.clear();
+  dg_ = std::move(g);
+  state_ = SfState::graph_set;
+}
+
+// StarForest::setup (starforest.cpp:82-161) on the device.
+void StarForest::setup_device() {
+  comm_->bind_device();
+  DevGraph& g = *dg_;
+  const int me = comm_->rank();
+  const int P = comm_->size();
+  const int64_t n = nleaves_;
+  Scratch sc;
+  const bool trace = std::getenv("SFG_TRACE_SETUP") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    SFG_CUDA(cudaStreamSynchronize(dstream()));
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[dsetup] %-28s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  };
+  const int gs = grid_for(n);
+
+  // Edge order: ascending leaf index (starforest.cpp:86-90), then stable by
+  // root rank — ords[i] = leaf ordinal of the i-th edge.
+  int64_t* ord = nullptr;  // leaf-index order, nullptr = identity
+  if (!g.ascending && n > 0) {
+    int64_t* iota = dalloc<int64_t>(n);
+    int64_t* keys = dalloc<int64_t>(n);
+    ord = dalloc<int64_t>(n);
+    k_iota<<<gs, kT, 0, dstream()>>>(iota, n);
+    sort_pairs(g.local, keys, iota, ord, n, 64);
+    SFG_CUDA(cudaStreamSynchronize(dstream()));
+    cudaFree(iota);
+    cudaFree(keys);
+  }
+  std::vector<int64_t> start(static_cast<size_t>(P) + 1, 0), cnt(static_cast<size_t>(P), 0);
+  if (P == 1 || n == 0) {
+    if (ord) {
+      g.ords = ord;
+    } else {
+      g.ords = dalloc<int64_t>(n);
+      if (n) k_iota<<<gs, kT, 0, dstream()>>>(g.ords, n);
+    }
+    cnt[0] = P == 1 ? n : 0;  // n == 0: every group empty
+  } else {
+    int32_t* kin = dalloc<int32_t>(n);
+    int32_t* kout = dalloc<int32_t>(n);
+    int64_t* vin = ord;
+    if (!vin) {
+      vin = dalloc<int64_t>(n);
+      k_iota<<<gs, kT, 0, dstream()>>>(vin, n);
+    }
+    k_gather<<<gs, kT, 0, dstream()>>>(g.rank, vin, kin, n);
+    g.ords = dalloc<int64_t>(n);
+    int bits = 0;
+    while ((1 << bits) < P) ++bits;
+    sort_pairs(kin, kout, vin, g.ords, n, bits);
+    int64_t* first = dalloc<int64_t>(P);
+    std::vector<int64_t> host_first(static_cast<size_t>(P), -1);
+    SFG_CUDA(cudaMemcpyAsync(first, host_first.data(), static_cast<size_t>(P) * 8, cudaMemcpyHostToDevice,
+                             dstream()));
+    k_key_starts<<<gs, kT, 0, dstream()>>>(kout, n, first);
+    SFG_CUDA(cudaMemcpyAsync(host_first.data(), first, static_cast<size_t>(P) * 8, cudaMemcpyDeviceToHost,
+                             dstream()));
+    SFG_CUDA(cudaStreamSynchronize(dstream()));
+    cudaFree(first);
+    cudaFree(kin);
+    cudaFree(kout);
+    cudaFree(vin);
+    int64_t next = n;
+    for (int r = P - 1; r >= 0; --r) {
+      if (host_first[static_cast<size_t>(r)] < 0) continue;
+      cnt[static_cast<size_t>(r)] = next - host_first[static_cast<size_t>(r)];
+      next = host_first[static_cast<size_t>(r)];
+    }
+  }
+  for (int r = 0; r < P; ++r) start[static_cast<size_t>(r) + 1] = start[static_cast<size_t>(r)] + cnt[static_cast<size_t>(r)];
+  SFG_CUDA(cudaGetLastError());
+  mark("order + group by rank");
+
+  if (g.local) {
+    g.ridx = dalloc<int64_t>(n);
+    if (n) k_gather<<<gs, kT, 0, dstream()>>>(g.local, g.ords, g.ridx, n);
+  } else {
+    g.ridx = g.ords;
+  }
+  // Discovery payload: root offsets in edge order (starforest.cpp:96-107).
+  int64_t* payload = dalloc<int64_t>(n);
+  if (n) k_gather<<<gs, kT, 0, dstream()>>>(g.off, g.ords, payload, n);
+  SFG_CUDA(cudaGetLastError());
+  std::vector<std::vector<uint8_t>> send(static_cast<size_t>(P));
+  for (int r = 0; r < P; ++r) {
+    if (r == me || cnt[static_cast<size_t>(r)] == 0) continue;
+    auto& b = send[static_cast<size_t>(r)];
+    b.resize(static_cast<size_t>(cnt[static_cast<size_t>(r)]) * 8);
+    SFG_CUDA(cudaMemcpyAsync(b.data(), payload + start[static_cast<size_t>(r)], b.size(),
+                             cudaMemcpyDeviceToHost, dstream()));
+  }
+  SFG_CUDA(cudaStreamSynchronize(dstream()));
+  mark("payload");
+  auto recv = P > 1 ? comm_->ctrl().alltoallv(std::move(send)) : std::vector<std::vector<uint8_t>>(1);
+  mark("discovery exchange");
+
+  // Leaf groups' items back to back: self first (never left HBM), then the
+  // received lists in ascending rank.
+  const int64_t nself = cnt[static_cast<size_t>(me)];
+  int64_t total = nself;
+  for (int r = 0; r < P; ++r)
+    if (r != me) {
+      SFG_REQUIRE(recv[static_cast<size_t>(r)].size() % 8 == 0, "malformed setup payload");
+      total += static_cast<int64_t>(recv[static_cast<size_t>(r)].size() / 8);
+    }
+  std::vector<int64_t> lstart(static_cast<size_t>(P), 0), lcnt(static_cast<size_t>(P), 0);
+  lcnt[static_cast<size_t>(me)] = nself;
+  if (P == 1) {
+    g.loffs = payload;
+  } else {
+    g.loffs = dalloc<int64_t>(total);
+    if (nself)
+      SFG_CUDA(cudaMemcpyAsync(g.loffs, payload + start[static_cast<size_t>(me)], static_cast<size_t>(nself) * 8,
+                               cudaMemcpyDeviceToDevice, dstream()));
+    int64_t at = nself;
+    for (int r = 0; r < P; ++r) {
+      if (r == me) continue;
+      const auto& b = recv[static_cast<size_t>(r)];
+      lstart[static_cast<size_t>(r)] = at;
+      lcnt[static_cast<size_t>(r)] = static_cast<int64_t>(b.size() / 8);
+      if (!b.empty())
+        SFG_CUDA(cudaMemcpyAsync(g.loffs + at, b.data(), b.size(), cudaMemcpyHostToDevice, dstream()));
+      at += lcnt[static_cast<size_t>(r)];
+    }
+    SFG_CUDA(cudaStreamSynchronize(dstream()));
+    cudaFree(payload);
+  }
+  recv.clear();
+  mark("receive");
+
+  // Groups in ascending rank, offsets validated (starforest.cpp:116-123),
+  // then the self group rotated to the head and every list classified.
+  std::vector<Group> roots, leaves;
+  for (int r = 0; r < P; ++r) {
+    if (cnt[static_cast<size_t>(r)] == 0) continue;
+    Group gr;
+    gr.rank = r;
+    gr.ditems = g.ords + start[static_cast<size_t>(r)];
+    gr.pat.count = cnt[static_cast<size_t>(r)];
+    roots.push_back(gr);
+  }
+  const int64_t nr = nroots_;
+  for (int r = 0; r < P; ++r) {
+    const int64_t m = lcnt[static_cast<size_t>(r)];
+    if (m == 0) continue;
+    const int64_t* items = g.loffs + lstart[static_cast<size_t>(r)];
+    const int64_t bad = find_first(m, [=] __device__(int64_t i) { return items[i] >= nr; }, sc);
+    SFG_REQUIRE(bad == m, "setup: leaf on rank " + std::to_string(r) + " references root offset " +
+                              std::to_string(bad < m ? read1(items + bad) : 0) + " but this rank has only " +
+                              std::to_string(nroots_) + " roots");
+    Group gl;
+    gl.rank = r;
+    gl.ditems = items;
+    gl.pat.count = m;
+    leaves.push_back(gl);
+  }
+  mark("validate");
+  auto self_to_head = [me](std::vector<Group>& v) {
+    auto it = std::find_if(v.begin(), v.end(), [me](const Group& x) { return x.rank == me; });
+    if (it != v.end()) std::rotate(v.begin(), it, it + 1);
+  };
+  self_to_head(roots);
+  self_to_head(leaves);
+  self_first_ = !roots.empty() && roots.front().rank == me;
+  for (auto& gr : roots) {
+    const int64_t* ip = g.ridx + (gr.ditems - g.ords);
+    gr.pat = analyze_dev(ip, gr.pat.count, sc);
+  }
+  mark("analyze root groups");
+  for (auto& gl : leaves) gl.pat = analyze_dev(gl.ditems, gl.pat.count, sc);
+  mark("analyze leaf groups");
+
+  root_groups_ = std::move(roots);
+  leaf_groups_ = std::move(leaves);
+  g.host_ready = false;
+  state_ = SfState::set_up;
+}
+
+// Host copies of a device-set graph and its groups, for the host-side
+// consumers (degrees, multi-SF, algebra, CSR build, group export).
+void StarForest::host_graph() const {
+  if (!dg_ || dg_->host_ready) return;
+  comm_->bind_device();
+  const DevGraph& g = *dg_;
+  const size_t n = static_cast<size_t>(nleaves_);
+  auto down = [](auto& dst, const auto* src, size_t cnt) {
+    dst.resize(cnt);
+    if (cnt)
+      SFG_CUDA(cudaMemcpyAsync(dst.data(), src, cnt * sizeof(*src), cudaMemcpyDeviceToHost, dstream()));
+  };
+  if (g.local) down(leaf_local_, g.local, n);
+  down(remote_rank_, g.rank, n);
+  down(remote_off_, g.off, n);
+  if (state_ == SfState::set_up) {
+    for (auto* gs : {&root_groups_, &leaf_groups_})
+      for (auto& gr : *gs) {
+        down(gr.items, gr.ditems, static_cast<size_t>(gr.count()));
+        if (gr.pat.kind == Pattern::indexed) down(gr.pat.idx, gr.pat.didx, static_cast<size_t>(gr.count()));
+      }
+  }
+  SFG_CUDA(cudaStreamSynchronize(dstream()));
+  dg_->host_ready = true;
+}
+
+}  // namespace sfg

@@ -151,6 +151,7 @@ struct Pattern {
   int64_t start = 0;
   int64_t dx = 0, dy = 0, dz = 0, s1 = 0, s2 = 0;  // affine
   HostVec<int64_t> idx;                             // indexed
+  const int64_t* didx = nullptr;  // indexed, device SetUp: the list in HBM (DevGraph-owned)
   bool has_duplicates = false;
   int64_t distinct = 0;  // number of distinct indices
   int64_t bound = 0;  // largest index + 1 (0 when empty)
@@ -303,6 +304,25 @@ struct Group {
   int rank = -1;
   HostVec<int64_t> items;  // root groups: leaf ordinals; leaf groups: root offsets
   Pattern pat;                 // root groups: leaf-index pattern; leaf groups: root pattern
+  const int64_t* ditems = nullptr;  // device SetUp: items in HBM (host copy made on demand)
+  int64_t count() const { return pat.count; }
+};
+
+// Graph and SetUp products of a forest whose graph was given in device
+// memory (set_graph_device). SetUp then runs on the GPU
+// (dsetup.cu); host copies of the groups are only made when a host-side
+// consumer (degrees, multi-SF, algebra, CSR build, group export) asks.
+struct DevGraph {
+  int device = -1;
+  int64_t* local = nullptr;  // leaf indices, nullptr = identity
+  int32_t* rank = nullptr;
+  int64_t* off = nullptr;
+  bool ascending = true;     // leaf indices strictly increasing
+  int64_t* ords = nullptr;   // root groups' items (leaf ordinals), groups back to back
+  int64_t* ridx = nullptr;   // their leaf indices (== ords when local is nullptr)
+  int64_t* loffs = nullptr;  // leaf groups' items (root offsets), groups back to back
+  bool host_ready = false;   // host copies made
+  ~DevGraph();
 };
 
 // Device-resident plan (built once per forest, on first use).
@@ -424,7 +444,14 @@ class StarForest {
 
   void set_graph(int64_t nroots, int64_t nleaves, const int64_t* leaf_local,
                  const int32_t* remote_rank, const int64_t* remote_off);
+  // Same contract, arrays in the communicator's device memory (dsetup.cu).
+  void set_graph_device(int64_t nroots, int64_t nleaves, const int64_t* leaf_local,
+                        const int32_t* remote_rank, const int64_t* remote_off);
   void setup(SetupAlg alg = SetupAlg::automatic);
+  bool device_graph() const { return dg_ != nullptr; }
+  // Host copies of a device-set graph and its groups (no-op otherwise).
+  void host_graph() const;
+  void setup_device();  // setup() of a device-set graph (dsetup.cu)
 
   Comm& comm() { return *comm_; }
   SfState state() const { return state_; }
@@ -459,11 +486,13 @@ class StarForest {
   int64_t nroots_ = 0, nleaves_ = 0, leaf_bound_ = 0;
   bool contiguous_leaves_ = true;
   bool has_local_ = false;
-  HostVec<int64_t> leaf_local_;
-  HostVec<int32_t> remote_rank_;
-  HostVec<int64_t> remote_off_;
-  std::vector<Group> root_groups_, leaf_groups_;
+  // mutable: host_graph() fills them lazily for device-set graphs
+  mutable HostVec<int64_t> leaf_local_;
+  mutable HostVec<int32_t> remote_rank_;
+  mutable HostVec<int64_t> remote_off_;
+  mutable std::vector<Group> root_groups_, leaf_groups_;
   bool self_first_ = false;
+  std::unique_ptr<DevGraph> dg_;
   std::unique_ptr<StarForest> multi_;
   std::unique_ptr<DevPlan> dev_;
   std::vector<std::unique_ptr<Staging>> staging_;
@@ -517,6 +546,12 @@ std::unique_ptr<OpHandle> scatter_begin(StarForest& sf, const Unit& u, const voi
 void scatter_end(OpHandle& h);
 
 DPat to_dpat(const Pattern& p, const int32_t* dev_idx);
+
+// Device SetUp helpers (dsetup.cu), on the current device, synchronous.
+// dst[i] = src[i] as int32; throws when a value exceeds the int32 range.
+void dev_narrow_index(const int64_t* src, int64_t n, int32_t* dst);
+// Whether any value in [0, bound) occurs twice across the lists.
+bool dev_any_repeat(const std::vector<std::pair<const int64_t*, int64_t>>& lists, int64_t bound);
 
 // ------------------------------------------------------- graph algebra
 // starforest.hpp:150-171 (algebra.cpp). Collective; results are set up

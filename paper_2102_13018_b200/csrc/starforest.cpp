@@ -148,11 +148,16 @@ void StarForest::set_graph(int64_t nroots, int64_t nleaves, const int64_t* leaf_
   multi_.reset();
   dev_.reset();
   staging_.clear();
+  dg_.reset();
   state_ = SfState::graph_set;
 }
 
 void StarForest::setup(SetupAlg alg) {
   require_state(SfState::graph_set, "setup");
+  if (dg_) {
+    setup_device();
+    return;
+  }
   (void)alg;  // dense and consensus discovery produce identical results
               // (exchange.hpp:30-32); both map to one sparse exchange here.
   const int me = comm_->rank();
@@ -304,6 +309,7 @@ bool StarForest::has_self_edges() const {
 
 std::vector<int64_t> StarForest::compute_degrees() const {
   require_state(SfState::set_up, "compute_degrees");
+  host_graph();
   std::vector<int64_t> degree(static_cast<size_t>(nroots_), 0);
   for (const auto& g : leaf_groups_)
     for (int64_t off : g.items) ++degree[static_cast<size_t>(off)];
@@ -315,6 +321,7 @@ std::vector<int64_t> StarForest::compute_degrees() const {
 StarForest& StarForest::multi_sf() {
   require_state(SfState::set_up, "multi_sf");
   if (multi_) return *multi_;
+  host_graph();
   const int P = comm_->size();
   const auto degrees = compute_degrees();
   std::vector<int64_t> next(degrees.size());
@@ -368,16 +375,16 @@ DevPlan& StarForest::dev() {
   const int me = comm_->rank();
   const bool force = comm_->config().force_remote;
 
-  // Collect the int32 arrays of every indexed pattern into one upload.
+  // Collect the int32 arrays of every indexed pattern into one blob: host
+  // lists are narrowed here and uploaded, device-SetUp lists (Pattern::didx)
+  // are narrowed on the device.
   std::vector<int32_t> host;
   std::vector<std::pair<const Pattern*, size_t>> idx_pats;
+  size_t blob_n = 0;
   auto reserve_pat = [&](const Pattern& p) {
     if (p.kind != Pattern::indexed) return;
-    idx_pats.push_back({&p, host.size()});
-    for (int64_t v : p.idx) {
-      SFG_REQUIRE(v <= kI32Max, "index exceeds the int32 range of device plans");
-      host.push_back(static_cast<int32_t>(v));
-    }
+    idx_pats.push_back({&p, blob_n});
+    blob_n += static_cast<size_t>(p.count);
   };
 
   const bool self = self_first_ && !force;
@@ -389,10 +396,28 @@ DevPlan& StarForest::dev() {
   for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size(); ++gi) reserve_pat(leaf_groups_[gi].pat);
 
   int32_t* dbase = nullptr;
-  if (!host.empty()) {
-    SFG_CUDA(cudaMalloc(&d->blob, host.size() * sizeof(int32_t)));
-    SFG_CUDA(cudaMemcpy(d->blob, host.data(), host.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  if (blob_n) {
+    SFG_CUDA(cudaMalloc(&d->blob, blob_n * sizeof(int32_t)));
     dbase = static_cast<int32_t*>(d->blob);
+    host.resize(blob_n);
+    bool any_host = false;
+    for (const auto& [pp, o] : idx_pats) {
+      if (pp->didx) {
+        dev_narrow_index(pp->didx, pp->count, dbase + o);
+        continue;
+      }
+      any_host = true;
+      for (int64_t i = 0; i < pp->count; ++i) {
+        const int64_t v = pp->idx[static_cast<size_t>(i)];
+        SFG_REQUIRE(v <= kI32Max, "index exceeds the int32 range of device plans");
+        host[o + static_cast<size_t>(i)] = static_cast<int32_t>(v);
+      }
+    }
+    if (any_host)
+      for (const auto& [pp, o] : idx_pats)
+        if (!pp->didx && pp->count)
+          SFG_CUDA(cudaMemcpy(dbase + o, host.data() + o, static_cast<size_t>(pp->count) * sizeof(int32_t),
+                              cudaMemcpyHostToDevice));
   }
   auto dpat = [&](const Pattern& p) {
     const int32_t* ptr = nullptr;
@@ -403,7 +428,7 @@ DevPlan& StarForest::dev() {
 
   if (self) {
     d->has_self = true;
-    d->n_self = static_cast<int64_t>(leaf_groups_.front().items.size());
+    d->n_self = leaf_groups_.front().count();
     d->self_root = dpat(leaf_groups_.front().pat);
     d->self_leaf = dpat(root_groups_.front().pat);
     d->self_root_dups = leaf_groups_.front().pat.has_duplicates;
@@ -412,7 +437,7 @@ DevPlan& StarForest::dev() {
   int64_t off = 0;
   for (size_t gi = self ? 1 : 0; gi < root_groups_.size(); ++gi) {
     const auto& g = root_groups_[gi];
-    const int64_t cnt = static_cast<int64_t>(g.items.size());
+    const int64_t cnt = g.count();
     d->rg.push_back({g.rank, cnt, off, dpat(g.pat), g.pat.is_contiguous(), g.pat.start, g.pat.distinct});
     off += cnt;
   }
@@ -420,7 +445,7 @@ DevPlan& StarForest::dev() {
   off = 0;
   for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size(); ++gi) {
     const auto& g = leaf_groups_[gi];
-    const int64_t cnt = static_cast<int64_t>(g.items.size());
+    const int64_t cnt = g.count();
     d->lg.push_back({g.rank, cnt, off, dpat(g.pat), g.pat.is_contiguous(), g.pat.start, g.pat.distinct});
     off += cnt;
   }
@@ -429,7 +454,12 @@ DevPlan& StarForest::dev() {
               "remote edge count exceeds the int32 range of device plans");
 
   // Does any root receive more than one remote contribution?
-  if (d->lg.size() > 0) {
+  if (d->lg.size() > 0 && dg_ && !dg_->host_ready) {
+    std::vector<std::pair<const int64_t*, int64_t>> lists;
+    for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size(); ++gi)
+      lists.push_back({leaf_groups_[gi].ditems, leaf_groups_[gi].count()});
+    d->remote_root_dups = dev_any_repeat(lists, nroots_);
+  } else if (d->lg.size() > 0) {
     std::vector<uint8_t> seen(static_cast<size_t>(nroots_), 0);
     for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size() && !d->remote_root_dups; ++gi)
       for (int64_t r : leaf_groups_[gi].items) {
@@ -451,6 +481,7 @@ DevPlan& StarForest::dev() {
 void StarForest::ensure_csr() {
   DevPlan& d = dev();
   if (d.csr_built) return;
+  host_graph();
   comm_->bind_device();
   const bool self = d.has_self;
   std::vector<int32_t> cnt_self(static_cast<size_t>(nroots_), 0), cnt_all(static_cast<size_t>(nroots_), 0);

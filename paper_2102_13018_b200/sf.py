@@ -385,6 +385,28 @@ class StarForest:
                                        ro.ctypes.data if ro.size else None))
         self._multi = None
 
+    def set_graph_device(self, nroots: int, nleaves: int, local, remote_rank, remote_off) -> None:
+        """set_graph with the arrays already in the communicator's device memory
+        (torch CUDA tensors: int64 leaf indices or None, int32 root ranks,
+        int64 root offsets); setup() then plans on the GPU."""
+        import torch
+
+        def ptr(t, dtype, name):
+            if t is None:
+                return None
+            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dtype and t.is_contiguous()):
+                raise Error(f"set_graph_device: {name} must be a contiguous CUDA {dtype} tensor")
+            if t.numel() != nleaves:
+                raise Error("set_graph: leaf_remote length does not match nleaves")
+            return t.data_ptr() if t.numel() else None
+        lp = ptr(local, torch.int64, "local")
+        if local is not None and lp is None:
+            lp = C.c_void_p(1)  # empty but present
+        _check(_lib().sfg_sf_set_graph_device(self._h, int(nroots), int(nleaves), lp,
+                                              ptr(remote_rank, torch.int32, "remote_rank"),
+                                              ptr(remote_off, torch.int64, "remote_off")))
+        self._multi = None
+
     def set_graph_spec(self, spec: GraphSpec) -> None:
         self.set_graph(spec.nroots, spec.nleaves, spec.local, remote_rank=spec.remote_rank,
                        remote_off=spec.remote_off)

@@ -19,13 +19,21 @@ def to_dev(a: np.ndarray):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
+def set_graph_device(f, spec):
+    """set_graph_device of a GraphSpec through CUDA copies of its arrays."""
+    loc = None if spec.local is None else to_dev(np.asarray(spec.local, np.int64))
+    f.set_graph_device(spec.nroots, spec.nleaves, loc, to_dev(np.asarray(spec.remote_rank, np.int32)),
+                       to_dev(np.asarray(spec.remote_off, np.int64)))
+
+
 def to_host(t) -> np.ndarray:
     return t.cpu().numpy()
 
 
 def run_gpu(specs, opkind: str, data: list[list[np.ndarray]], op: str = "replace",
             blocklen: int = 1, config: sf.CommConfig | None = None, devices=None,
-            setup_alg=sf.SetupAlg.automatic, two_phase: bool = False):
+            setup_alg=sf.SetupAlg.automatic, two_phase: bool = False,
+            device_graph: bool = False):
     """data: per-buffer list of per-rank arrays, in the op's argument order:
     bcast (root, leaf) reduce (leaf, root) fetch_and_op (root, leaf, update)
     gather (leaf, multiroot) scatter (multiroot, leaf). Returns the same
@@ -42,7 +50,10 @@ def run_gpu(specs, opkind: str, data: list[list[np.ndarray]], op: str = "replace
 
         r = comm.rank()
         f = sf.StarForest(comm)
-        f.set_graph_spec(specs[r])
+        if device_graph:
+            set_graph_device(f, specs[r])
+        else:
+            f.set_graph_spec(specs[r])
         f.setup(setup_alg)
         bufs = [to_dev(d[r]) for d in data]
         stream = torch.cuda.Stream()
