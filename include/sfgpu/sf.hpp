@@ -182,6 +182,12 @@ class StarForest {
                                    rr.data(), ro.data()));
   }
   void set_graph(const GraphSpec& s) { set_graph(s.nroots, s.nleaves, s.local, s.remote); }
+  // The graph already in the communicator's device memory:
+  // leaf_local may be nullptr; setup() then plans on the GPU.
+  void set_graph_device(std::int64_t nroots, std::int64_t nleaves, const std::int64_t* leaf_local,
+                        const std::int32_t* remote_rank, const std::int64_t* remote_off) {
+    detail::check(sfg_sf_set_graph_device(h_, nroots, nleaves, leaf_local, remote_rank, remote_off));
+  }
   void setup(SetupAlg alg = SetupAlg::automatic) { detail::check(sfg_sf_setup(h_, static_cast<int>(alg))); }
 
   SfState state() const { return static_cast<SfState>(info().state); }
