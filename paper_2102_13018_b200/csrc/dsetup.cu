@@ -20,6 +20,8 @@
 // blocking in the reference too). Group items stay in HBM; host copies are
 // made on demand by host_graph() for host-side consumers.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_run_length_encode.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -306,6 +308,93 @@ Pattern analyze_dev(const int64_t* idx, int64_t n, Scratch& sc) {
   p.distinct = count_distinct_dev(idx, n, got[0], got[1], sc);
   p.has_duplicates = p.distinct < n;
   return p;
+}
+
+// ---------------------------------------------------------------- CSR build
+// Root-sorted CSR of every contribution (StarForest::ensure_csr): one stable
+// radix sort of (root, entry) pairs given in fold order, run-length encoding
+// for the root list, binary searches for the self/remote split and the L2
+// piece table, and a compaction for the remote-only view.
+
+__global__ void k_csr_fill(const int64_t* keys, const int64_t* vals, int64_t n, int64_t base, int32_t* kout,
+                           int32_t* vout, u64* bad) {
+  u64 first = ~0ull;
+  for (int64_t i = blockIdx.x * int64_t(kT) + threadIdx.x; i < n; i += int64_t(gridDim.x) * kT) {
+    kout[i] = static_cast<int32_t>(keys[i]);
+    if (vals) {
+      const int64_t v = vals[i];
+      if (v > kI32Max && first == ~0ull) first = static_cast<u64>(i);
+      vout[i] = static_cast<int32_t>(v);
+    } else {
+      vout[i] = static_cast<int32_t>(-(base + i) - 1);
+    }
+  }
+  block_min_to(first, bad);
+}
+
+// Per root q: split = first remote (negative) entry; ptab row = first self
+// entry at or beyond b * piece for b = 1..cols (self entries ascend).
+__global__ void k_csr_split(const int32_t* off, const int32_t* ent, int64_t nq, int32_t* split, int32_t* ptab,
+                            int cols, int64_t piece) {
+  for (int64_t q = blockIdx.x * int64_t(kT) + threadIdx.x; q < nq; q += int64_t(gridDim.x) * kT) {
+    int32_t lo = off[q], hi = off[q + 1];
+    while (lo < hi) {
+      const int32_t mid = lo + (hi - lo) / 2;
+      if (ent[mid] >= 0) lo = mid + 1; else hi = mid;
+    }
+    split[q] = lo;
+    for (int b = 1; b <= cols; ++b) {
+      int32_t a = off[q], e = lo;
+      const int64_t v = b * piece;
+      while (a < e) {
+        const int32_t mid = a + (e - a) / 2;
+        if (ent[mid] < v) a = mid + 1; else e = mid;
+      }
+      ptab[q * cols + (b - 1)] = a;
+    }
+  }
+}
+
+__global__ void k_csr_remote_counts(const int32_t* off, const int32_t* split, int64_t nq, int32_t* flag,
+                                    int32_t* rcnt) {
+  for (int64_t q = blockIdx.x * int64_t(kT) + threadIdx.x; q < nq; q += int64_t(gridDim.x) * kT) {
+    const int32_t r = off[q + 1] - split[q];
+    flag[q] = r > 0;
+    rcnt[q] = r;
+  }
+}
+
+__global__ void k_csr_remote_view(const int32_t* roots, const int32_t* off, const int32_t* split,
+                                  const int32_t* ent, int64_t nq, const int32_t* fpos, const int32_t* rpos,
+                                  int32_t* rroots, int32_t* roffs, int32_t* rent, int32_t* clo, int32_t* chi,
+                                  uint32_t* cbits, u64* centries) {
+  u64 ce = 0;
+  for (int64_t q = blockIdx.x * int64_t(kT) + threadIdx.x; q < nq; q += int64_t(gridDim.x) * kT) {
+    const int32_t a = split[q], b = off[q + 1];
+    if (a == b) continue;
+    const int32_t k = fpos[q], p = rpos[q];
+    rroots[k] = roots[q];
+    roffs[k] = p;
+    for (int32_t j = a; j < b; ++j) rent[p + (j - a)] = ent[j];
+    if (clo) {
+      clo[k] = off[q];
+      chi[k] = b;
+      ce += static_cast<u64>(b - off[q]);
+      if (a > off[q]) atomicOr(&cbits[roots[q] >> 5], 1u << (roots[q] & 31));
+    }
+  }
+  for (int o = 16; o; o >>= 1) ce += __shfl_xor_sync(0xffffffffu, ce, o);
+  if ((threadIdx.x & 31) == 0 && ce) atomicAdd(centries, ce);
+}
+
+template <class T>
+void excl_sum(const T* in, T* out, int64_t n) {
+  size_t tmp = 0;
+  SFG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, dstream()));
+  void* t = nullptr;
+  SFG_CUDA(cudaMallocAsync(&t, tmp, dstream()));
+  SFG_CUDA(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, n, dstream()));
+  SFG_CUDA(cudaFreeAsync(t, dstream()));
 }
 
 }  // namespace
@@ -637,6 +726,119 @@ void StarForest::host_graph() const {
   }
   SFG_CUDA(cudaStreamSynchronize(dstream()));
   dg_->host_ready = true;
+}
+
+void dev_csr_fill(const int64_t* keys, const int64_t* vals, int64_t n, int64_t base, int32_t* kout,
+                  int32_t* vout) {
+  if (n <= 0) return;
+  Scratch sc;
+  k_fill<<<1, 32, 0, dstream()>>>(sc.v, 1, ~0ull);
+  k_csr_fill<<<grid_for(n), kT, 0, dstream()>>>(keys, vals, n, base, kout, vout, sc.v);
+  SFG_CUDA(cudaGetLastError());
+  SFG_REQUIRE(read1(sc.v) == ~0ull, "leaf index exceeds the int32 range of device plans");
+}
+
+void dev_build_csr(DevPlan& d, int32_t* key, int32_t* val, int64_t total, int64_t n_self, int64_t nroots,
+                   int64_t leaf_bound, bool self) {
+  SFG_REQUIRE(total <= kI32Max, "CSR exceeds the int32 range of device plans");
+  Scratch sc;
+  int bits = 1;
+  while (bits < 31 && (int64_t(1) << bits) < nroots) ++bits;
+  int32_t* skey = dalloc<int32_t>(total);
+  int32_t* ent = dalloc<int32_t>(total);
+  if (total) sort_pairs(key, skey, val, ent, total, bits);
+  // roots + run lengths
+  int32_t* roots = dalloc<int32_t>(total + 1);
+  int32_t* cnts = dalloc<int32_t>(total + 1);
+  int64_t nq = 0;
+  if (total) {
+    int64_t* nruns = reinterpret_cast<int64_t*>(sc.v + 4);
+    size_t tmp = 0;
+    SFG_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tmp, skey, roots, cnts, nruns, total, dstream()));
+    void* t = nullptr;
+    SFG_CUDA(cudaMallocAsync(&t, tmp, dstream()));
+    SFG_CUDA(cub::DeviceRunLengthEncode::Encode(t, tmp, skey, roots, cnts, nruns, total, dstream()));
+    SFG_CUDA(cudaFreeAsync(t, dstream()));
+    nq = read1(nruns);
+  }
+  cudaFree(skey);
+  // offs: exclusive sum over nq + 1 counts (the extra one set to 0 -> total)
+  int32_t* offs = dalloc<int32_t>(nq + 1);
+  SFG_CUDA(cudaMemsetAsync(cnts + nq, 0, sizeof(int32_t), dstream()));
+  excl_sum(cnts, offs, nq + 1);
+
+  constexpr int64_t kPiece = int64_t(1) << 21;
+  const int64_t np_max = (leaf_bound + kPiece - 1) / kPiece;
+  const int64_t mean_deg = nq ? total / nq : 0;
+  const bool tiled = np_max >= 3 && mean_deg >= 8 && n_self > 0;
+  const int cols = tiled ? static_cast<int>(np_max - 1) : 0;
+  int32_t* split = dalloc<int32_t>(nq);
+  int32_t* ptab = dalloc<int32_t>(nq * cols);
+  if (nq) k_csr_split<<<grid_for(nq), kT, 0, dstream()>>>(offs, ent, nq, split, ptab, cols, kPiece);
+
+  // remote-only view
+  int32_t* flag = dalloc<int32_t>(nq + 1);
+  int32_t* rcnt = dalloc<int32_t>(nq + 1);
+  int32_t* fpos = dalloc<int32_t>(nq + 1);
+  int32_t* rpos = dalloc<int32_t>(nq + 1);
+  SFG_CUDA(cudaMemsetAsync(flag + nq, 0, sizeof(int32_t), dstream()));
+  SFG_CUDA(cudaMemsetAsync(rcnt + nq, 0, sizeof(int32_t), dstream()));
+  if (nq) k_csr_remote_counts<<<grid_for(nq), kT, 0, dstream()>>>(offs, split, nq, flag, rcnt);
+  excl_sum(flag, fpos, nq + 1);
+  excl_sum(rcnt, rpos, nq + 1);
+  const int64_t rn = read1(fpos + nq);
+  const int64_t rtotal = read1(rpos + nq);
+  const int64_t nbits = self ? (nroots + 31) / 32 : 0;
+  const int64_t ncl = self ? rn : 0;
+
+  const int64_t words = nq + (nq + 1) + nq + total + rn + (rn + 1) + rtotal + nq * cols + 2 * ncl + nbits;
+  if (words) SFG_CUDA(cudaMalloc(&d.csr_blob, static_cast<size_t>(words) * 4));
+  int32_t* p = static_cast<int32_t*>(d.csr_blob);
+  auto take = [&](int64_t n) {
+    int32_t* q = p;
+    p += n;
+    return q;
+  };
+  auto d2d = [&](int32_t* dst, const int32_t* src, int64_t n) {
+    if (n) SFG_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToDevice, dstream()));
+  };
+  d.csr_roots = take(nq);
+  d2d(d.csr_roots, roots, nq);
+  d.csr_off = take(nq + 1);
+  d2d(d.csr_off, offs, nq + 1);
+  d.csr_split = take(nq);
+  d2d(d.csr_split, split, nq);
+  d.csr_ent = take(total);
+  d2d(d.csr_ent, ent, total);
+  d.rcsr_roots = take(rn);
+  d.rcsr_off = take(rn + 1);
+  d.rcsr_ent = take(rtotal);
+  d.csr_ptab = take(nq * cols);
+  d2d(d.csr_ptab, ptab, nq * cols);
+  if (!tiled) d.csr_ptab = nullptr;
+  d.ccsr_lo = take(ncl);
+  d.ccsr_hi = take(ncl);
+  uint32_t* cb = reinterpret_cast<uint32_t*>(take(nbits));
+  if (nbits) SFG_CUDA(cudaMemsetAsync(cb, 0, static_cast<size_t>(nbits) * 4, dstream()));
+  d.coupled_bits = self ? cb : nullptr;
+  d2d(d.rcsr_off + rn, rpos + nq, 1);
+  k_fill<<<1, 32, 0, dstream()>>>(sc.v, 1, 0);
+  if (nq)
+    k_csr_remote_view<<<grid_for(nq), kT, 0, dstream()>>>(roots, offs, split, ent, nq, fpos, rpos, d.rcsr_roots,
+                                                          d.rcsr_off, d.rcsr_ent, self ? d.ccsr_lo : nullptr,
+                                                          self ? d.ccsr_hi : nullptr, cb, sc.v);
+  SFG_CUDA(cudaGetLastError());
+  d.ccsr_entries += static_cast<int64_t>(read1(sc.v));
+  for (int32_t* b : {ent, roots, cnts, offs, split, ptab, flag, rcnt, fpos, rpos})
+    if (b) cudaFree(b);
+  if (tiled) {
+    d.csr_np_max = static_cast<int32_t>(np_max);
+    d.csr_piece_leaves = kPiece;
+  }
+  d.csr_n = nq;
+  d.csr_self_entries = self ? n_self : 0;
+  d.csr_remote_entries = total - d.csr_self_entries;
+  d.rcsr_n = rn;
 }
 
 }  // namespace sfg

@@ -550,6 +550,13 @@ DPat to_dpat(const Pattern& p, const int32_t* dev_idx);
 // Device SetUp helpers (dsetup.cu), on the current device, synchronous.
 // dst[i] = src[i] as int32; throws when a value exceeds the int32 range.
 void dev_narrow_index(const int64_t* src, int64_t n, int32_t* dst);
+// CSR build (StarForest::ensure_csr): keys/vals to int32 pairs (vals ==
+// nullptr: remote entries -(base+i)-1), then the root-sorted CSR into d.
+void dev_csr_fill(const int64_t* keys, const int64_t* vals, int64_t n, int64_t base, int32_t* kout,
+                  int32_t* vout);
+struct DevPlan;
+void dev_build_csr(DevPlan& d, int32_t* key, int32_t* val, int64_t total, int64_t n_self, int64_t nroots,
+                   int64_t leaf_bound, bool self);
 // Whether any value in [0, bound) occurs twice across the lists.
 bool dev_any_repeat(const std::vector<std::pair<const int64_t*, int64_t>>& lists, int64_t bound);
 
