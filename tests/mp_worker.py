@@ -14,7 +14,7 @@ import torch.distributed as dist  # noqa: E402
 
 from oracle import oracle as O  # noqa: E402
 from paper_2102_13018_b200 import graphs, sf  # noqa: E402
-from tests.helpers import assert_same, rank_data  # noqa: E402
+from tests.helpers import assert_same, rank_data, set_graph_device  # noqa: E402
 
 
 def main():
@@ -137,6 +137,25 @@ def main():
                     dist.broadcast_object_list(obj, src=0)
                     cur = obj[0]
                 del g
+            if deterministic:
+                # Device SetUp (dsetup.cu) across processes: the same plan as
+                # the host planner, and the same Bcast / Reduce results.
+                fd = sf.StarForest(comm)
+                set_graph_device(fd, specs[rank])
+                fd.setup()
+                same = (fd.two_sided() == f.two_sided()
+                        and [g.pattern for g in fd.root_groups()] == [g.pattern for g in f.root_groups()]
+                        and [g.pattern for g in fd.leaf_groups()] == [g.pattern for g in f.leaf_groups()])
+                lb2 = dev(leaves[rank])
+                sf.bcast(fd, u, dev(roots[rank]), lb2, sf.ReduceOp.replace)
+                rb2 = dev(roots[rank])
+                sf.reduce(fd, u, dev(leaves[rank]), rb2, sf.ReduceOp.sum)
+                same = same and torch.equal(lb2, lb) and torch.equal(rb2.view(torch.int64), rb.view(torch.int64))
+                flags = [None] * world
+                dist.all_gather_object(flags, same)
+                if rank == 0 and not all(flags):
+                    fails.append(f"{name} device setup differs on ranks {[i for i, x in enumerate(flags) if not x]}")
+                del fd
             del f
         comm.close()
     dist.barrier()
