@@ -889,6 +889,26 @@ int launch_segments(LaunchParams& p, ElemType t, int op, cudaStream_t stream) {
   return 1;
 }
 
+__global__ void quiesce_kernel(const __grid_constant__ QuiesceParams q, unsigned long long timeout_ns) {
+  const int i = threadIdx.x;
+  if (i >= q.n) return;
+  const unsigned long long t0 = global_ns();
+  const unsigned long long need = *q.count[i];
+  while (ld_acquire_sys(q.flag[i]) < need) {
+    __nanosleep(256);
+    if (global_ns() - t0 > timeout_ns) {
+      printf("sfgpu p2p: teardown gave up waiting for a peer acknowledgement (%llu < %llu)\n",
+             ld_acquire_sys(q.flag[i]), need);
+      return;
+    }
+  }
+}
+
+void launch_quiesce(const QuiesceParams& q, double timeout_s, cudaStream_t s) {
+  if (q.n <= 0) return;
+  quiesce_kernel<<<1, QuiesceParams::kMax, 0, s>>>(q, static_cast<unsigned long long>(timeout_s * 1e9));
+}
+
 void launch_digest(const void* p, size_t bytes, unsigned long long* out_dev, cudaStream_t s) {
   cudaMemsetAsync(out_dev, 0, sizeof(unsigned long long), s);
   if (bytes == 0) return;

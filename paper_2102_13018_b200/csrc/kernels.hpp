@@ -163,6 +163,17 @@ enum class ElemType : int32_t { u8, u16, u32, u64, i32, i64, f64 };
 // Returns number of kernel launches issued (0 or 1 per call).
 int launch_segments(LaunchParams& p, ElemType t, int op, cudaStream_t stream);
 
+// p2p teardown: wait until every message this slot sent was acknowledged
+// (flag[i] >= *count[i]), so no peer still writes into the slot when it is
+// freed. Gives up with a warning after timeout_s (a dead peer).
+struct QuiesceParams {
+  static constexpr int kMax = 3 * kMaxPeers;
+  int n = 0;
+  const unsigned long long* flag[kMax];
+  const unsigned long long* count[kMax];
+};
+void launch_quiesce(const QuiesceParams& q, double timeout_s, cudaStream_t s);
+
 // Order-independent 64-bit digest of a device buffer (debug checksum).
 void launch_digest(const void* p, size_t bytes, unsigned long long* out_dev, cudaStream_t s);
 

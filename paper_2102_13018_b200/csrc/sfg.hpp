@@ -472,6 +472,7 @@ class StarForest {
   // device side
   DevPlan& dev();
   void ensure_csr();
+  void ensure_csr_host();
   Staging* acquire_staging(size_t ub, cudaStream_t stream);
   void release_staging(Staging* s, cudaStream_t stream);
   void p2p_attach(Staging& s);  // collective: allocate the slot, map it into the neighbors

@@ -55,6 +55,21 @@ DevPlan::~DevPlan() {
 }
 
 Staging::~Staging() {
+  static const bool no_quiesce = std::getenv("SFG_P2P_NO_QUIESCE") != nullptr;  // ablation
+  if (slot_mem && flags && !no_quiesce) {
+    // Peers acknowledge my puts by writing into this slot after their
+    // unpacks; wait for the last acknowledgement before freeing it.
+    QuiesceParams q;
+    for (int g = 0; g < 3; ++g)
+      for (int r = 0; r < nranks && r < static_cast<int>(peers.size()); ++r)
+        if (peers[static_cast<size_t>(r)].base && q.n < QuiesceParams::kMax) {
+          q.flag[q.n] = free_flag(g, r);
+          q.count[q.n] = sent(g, r);
+          ++q.n;
+        }
+    launch_quiesce(q, 10.0, cudaStreamPerThread);
+    cudaStreamSynchronize(cudaStreamPerThread);
+  }
   for (auto& p : peers)
     if (p.ipc && p.base) cudaIpcCloseMemHandle(p.base);
   if (slot_mem) {
@@ -482,6 +497,11 @@ DevPlan& StarForest::dev() {
 void StarForest::ensure_csr() {
   DevPlan& d = dev();
   if (d.csr_built) return;
+  static const bool host_csr = std::getenv("SFG_HOST_CSR") != nullptr;
+  if (host_csr) {
+    ensure_csr_host();
+    return;
+  }
   comm_->bind_device();
   PhaseTimer pt;
   const bool self = d.has_self;
@@ -542,6 +562,131 @@ void StarForest::ensure_csr() {
   if (val) cudaFree(val);
   d.csr_built = true;
   pt.mark("csr build");
+}
+
+// Host-built CSR (the round-1 implementation), kept for bisecting the
+// device build: SFG_HOST_CSR=1.
+void StarForest::ensure_csr_host() {
+  DevPlan& d = dev();
+  host_graph();
+  comm_->bind_device();
+  const bool self = d.has_self;
+  std::vector<int32_t> cnt_self(static_cast<size_t>(nroots_), 0), cnt_all(static_cast<size_t>(nroots_), 0);
+  if (self)
+    for (int64_t r : leaf_groups_.front().items) {
+      ++cnt_self[static_cast<size_t>(r)];
+      ++cnt_all[static_cast<size_t>(r)];
+    }
+  for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size(); ++gi)
+    for (int64_t r : leaf_groups_[gi].items) ++cnt_all[static_cast<size_t>(r)];
+
+  std::vector<int32_t> roots, offs, split;
+  std::vector<int64_t> cursor(static_cast<size_t>(nroots_), -1);
+  int64_t total = 0;
+  for (int64_t r = 0; r < nroots_; ++r) {
+    const int32_t c = cnt_all[static_cast<size_t>(r)];
+    if (c == 0) continue;
+    cursor[static_cast<size_t>(r)] = total;
+    roots.push_back(static_cast<int32_t>(r));
+    offs.push_back(static_cast<int32_t>(total));
+    split.push_back(static_cast<int32_t>(total + cnt_self[static_cast<size_t>(r)]));
+    total += c;
+    SFG_REQUIRE(total <= kI32Max, "CSR exceeds the int32 range of device plans");
+  }
+  offs.push_back(static_cast<int32_t>(total));
+  std::vector<int32_t> ent(static_cast<size_t>(total));
+  if (self) {
+    const auto& lg = leaf_groups_.front();
+    const auto& rg = root_groups_.front();
+    for (size_t i = 0; i < lg.items.size(); ++i) {
+      const int64_t leaf = leaf_index(rg.items[i]);
+      SFG_REQUIRE(leaf <= kI32Max, "leaf index exceeds the int32 range of device plans");
+      ent[static_cast<size_t>(cursor[static_cast<size_t>(lg.items[i])]++)] = static_cast<int32_t>(leaf);
+    }
+  }
+  size_t k = 0;
+  for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size(); ++gi, ++k) {
+    const auto& g = leaf_groups_[gi];
+    const int64_t base = d.lg[k].stage_off;
+    for (size_t i = 0; i < g.items.size(); ++i)
+      ent[static_cast<size_t>(cursor[static_cast<size_t>(g.items[i])]++)] =
+          static_cast<int32_t>(-(base + static_cast<int64_t>(i)) - 1);
+  }
+  d.csr_n = static_cast<int64_t>(roots.size());
+  d.csr_self_entries = self ? static_cast<int64_t>(leaf_groups_.front().items.size()) : 0;
+  d.csr_remote_entries = total - d.csr_self_entries;
+
+  // L2 tiling (kernels.cu run_csr_warp): where the leaf array the self
+  // contributions gather from is several times larger than L2, record per
+  // root the first self entry at or beyond each multiple of kPiece leaves.
+  constexpr int64_t kPiece = int64_t(1) << 21;
+  std::vector<int32_t> ptab;
+  const int64_t np_max = (leaf_bound_ + kPiece - 1) / kPiece;
+  const int64_t mean_deg = roots.empty() ? 0 : total / static_cast<int64_t>(roots.size());
+  if (np_max >= 3 && mean_deg >= 8 && d.csr_self_entries > 0) {
+    const int64_t cols = np_max - 1;
+    ptab.resize(roots.size() * static_cast<size_t>(cols));
+    for (size_t q = 0; q < roots.size(); ++q) {
+      int64_t j = offs[q];
+      const int64_t end = split[q];
+      for (int64_t b = 1; b <= cols; ++b) {
+        while (j < end && ent[static_cast<size_t>(j)] < b * kPiece) ++j;
+        ptab[q * static_cast<size_t>(cols) + static_cast<size_t>(b - 1)] = static_cast<int32_t>(j);
+      }
+    }
+    d.csr_np_max = static_cast<int32_t>(np_max);
+    d.csr_piece_leaves = kPiece;
+  }
+
+  // Remote-only view: the (usually few) roots with remote contributions, so
+  // the End-side fold does not walk every root of the forest.
+  std::vector<int32_t> rroots, roffs, rent, clo, chi;
+  std::vector<uint32_t> cbits;
+  if (self) cbits.assign(static_cast<size_t>((nroots_ + 31) / 32), 0u);
+  for (size_t q = 0; q < roots.size(); ++q) {
+    const int32_t a = split[q], b = offs[q + 1];
+    if (a == b) continue;
+    rroots.push_back(roots[q]);
+    roffs.push_back(static_cast<int32_t>(rent.size()));
+    rent.insert(rent.end(), ent.begin() + a, ent.begin() + b);
+    if (self) {
+      clo.push_back(offs[q]);
+      chi.push_back(b);
+      d.ccsr_entries += b - offs[q];
+      if (a > offs[q]) cbits[static_cast<size_t>(roots[q]) >> 5] |= 1u << (roots[q] & 31);
+    }
+  }
+  roffs.push_back(static_cast<int32_t>(rent.size()));
+  d.rcsr_n = static_cast<int64_t>(rroots.size());
+
+  const size_t bytes = (roots.size() + offs.size() + split.size() + ent.size() + rroots.size() +
+                        roffs.size() + rent.size() + ptab.size() + clo.size() + chi.size() +
+                        cbits.size()) * sizeof(int32_t);
+  if (bytes) {
+    SFG_CUDA(cudaMalloc(&d.csr_blob, bytes));
+    auto* p = static_cast<int32_t*>(d.csr_blob);
+    auto put = [&](const std::vector<int32_t>& v, int32_t*& dst) {
+      dst = p;
+      if (!v.empty()) SFG_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+      p += v.size();
+    };
+    put(roots, d.csr_roots);
+    put(offs, d.csr_off);
+    put(split, d.csr_split);
+    put(ent, d.csr_ent);
+    put(rroots, d.rcsr_roots);
+    put(roffs, d.rcsr_off);
+    put(rent, d.rcsr_ent);
+    put(ptab, d.csr_ptab);
+    if (ptab.empty()) d.csr_ptab = nullptr;
+    put(clo, d.ccsr_lo);
+    put(chi, d.ccsr_hi);
+    std::vector<int32_t> cb(cbits.begin(), cbits.end());
+    int32_t* cbp = nullptr;
+    put(cb, cbp);
+    d.coupled_bits = cbits.empty() ? nullptr : reinterpret_cast<uint32_t*>(cbp);
+  }
+  d.csr_built = true;
 }
 
 Staging* StarForest::acquire_staging(size_t ub, cudaStream_t stream) {

@@ -115,6 +115,47 @@ def test_p2p_outstanding_handles_and_slot_reuse():
 
 
 @need2
+def test_p2p_teardown_waits_for_peer_acknowledgements():
+    """A rank that is done first must not free its staging slot while a slower
+    peer's unpack still has to acknowledge the puts it received (the peer's
+    acknowledgement is a store into that slot over NVLink): Staging teardown
+    waits for every acknowledgement."""
+    import time
+
+    import torch
+
+    n = min(ngpu(), 4)
+    specs = graphs.random_graph_specs(11, n, 200)
+    roots = rank_data(specs, 2, np.float64, 1, 100, "root")
+    leaves = rank_data(specs, 2, np.float64, 1, 200, "leaf")
+    want = O.bcast(specs, roots, leaves)
+    u = sf.Unit(sf.Kind.float64)
+
+    def body(comm):
+        r = comm.rank()
+        out = []
+        for it in range(8):
+            f = sf.StarForest(comm)
+            f.set_graph_spec(specs[r])
+            f.setup()
+            root = torch.from_numpy(roots[r]).cuda()
+            leaf = torch.from_numpy(leaves[r]).cuda()
+            st = torch.cuda.current_stream()
+            h = sf.bcast_begin(f, u, root, leaf, sf.ReduceOp.replace, st)
+            if r == n - 1:
+                time.sleep(0.02)  # the others finish and tear down first
+            sf.bcast_end(h)
+            out.append(leaf.cpu().numpy())
+            del h, f
+        torch.cuda.synchronize()
+        return out
+
+    got = sf.run_ranks(sf.CommConfig(nranks=n, backend="p2p"), body, devices=list(range(n)))
+    for it in range(8):
+        assert_same([g[it] for g in got], want, what=f"iter {it}")
+
+
+@need2
 def test_p2p_stress_visibility():
     """Every put is followed by a single system-scope release from the last
     CTA (kernels.cu cta_arrive): 300 back-to-back Bcast+Reduce rounds on a
