@@ -24,6 +24,7 @@
 // reference in both modes (free-order mode keeps an atomics path behind
 // SFG_FREE_ORDER_ATOMICS, pack.cpp:47-58 "atomics" mode).
 #include <algorithm>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -454,7 +455,8 @@ bool use_p2p(const OpHandle& h) { return h.sf->comm().p2p() && h.stg && h.stg->f
 // its stream between Begin and End (the local scatter, or its own work, e.g.
 // the diagonal SpMV product) overlaps the exchange; a small local scatter
 // joins the puts' launch instead.
-void p2p_begin(OpHandle& h, Launch& pack, Launch& local) {
+void p2p_begin(OpHandle& h, Launch& pack, Launch& local,
+               const std::function<void(Launch&)>& append_last = nullptr) {
   Comm& c = h.sf->comm();
   h.xfer = pack.p.nseg > 0;
   h.forked = false;
@@ -470,10 +472,12 @@ void p2p_begin(OpHandle& h, Launch& pack, Launch& local) {
     for (int i = 0; i < local.p.nseg; ++i)
       pack.add(local.p.seg[i], local.csr_entries[i], local.distinct_src[i], local.distinct_dst[i]);
     pack.tag = tag_of(h, 0);
+    if (append_last) append_last(pack);
     pack.run(h.unit, h.op, cs);
   } else {
     pack.tag = tag_of(h, 2);
     local.tag = tag_of(h, 3);
+    if (append_last) append_last(pack);
     pack.run(h.unit, h.op, cs);
     local.run(h.unit, h.op, h.stream);
   }
@@ -551,7 +555,28 @@ void begin_root_to_leaf(OpHandle& h) {
     if (d.has_self)
       local.add(pair_seg(d.self_root, BUF_ROOT, d.self_leaf, BUF_LEAF, d.n_self, replace), 0,
                 d.self_root_distinct);
-    p2p_begin(h, pack, local);
+    // The unpack of the incoming messages joins the put launch, after the
+    // puts and the local scatter (their CTAs dispatch first, so spinning
+    // unpack CTAs never hold back work they wait on): one launch per
+    // exchange. Leafdata belongs to the operation between Begin and End.
+    static const bool no_fuse = std::getenv("SFG_P2P_NO_FUSED_UNPACK") != nullptr;
+    h.fused_unpack = false;
+    auto fuse = [&](Launch& L) {
+      const size_t ng = d.rg.size();
+      if (no_fuse || ng == 0 || L.p.nseg + ng > static_cast<size_t>(kMaxSegs) ||
+          L.nwait + ng > static_cast<size_t>(kMaxPeers) || L.p.ndone + ng > static_cast<size_t>(kMaxPeers))
+        return;
+      const auto bits = add_receives(h, L, d.rg, 0, true);
+      for (size_t k = 0; k < ng; ++k) {
+        const auto& g = d.rg[k];
+        DSeg sg = pair_seg(contig(g.stage_off), BUF_LEAF_STAGE, g.pat, BUF_LEAF, g.n, replace);
+        sg.wait_mask = bits[k];
+        L.add(sg);
+        counters().unpack_copies++;
+      }
+      h.fused_unpack = true;
+    };
+    p2p_begin(h, pack, local, fuse);
     return;
   }
 
@@ -594,6 +619,10 @@ void end_root_to_leaf(OpHandle& h) {
   // concurrently with a local scatter still running on the caller's stream;
   // the caller's stream then joins.
   Comm& c = sf.comm();
+  if (use_p2p(h) && h.fused_unpack) {
+    p2p_join(h);
+    return;
+  }
   if (use_p2p(h)) {
     const auto bits = add_receives(h, L, d.rg, 0, true);
     for (size_t k = 0; k < d.rg.size(); ++k) {
