@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--sample-steps", type=int, default=10)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-device-setup", action="store_true")
     p.add_argument("--dims", type=lambda v: tuple(int(x) for x in v.split(",")), default=None,
                    help="process grid px,py,pz (default: 1x1x2 / 1x2x2 / 2x2x2 for 2 / 4 / 8 GPUs)")
     p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
@@ -300,10 +301,42 @@ def ours(args, rank, world, local):
     geo = graphs.G2L(args.N, world, rank, dims=args.dims)
     gen_s = time.perf_counter() - t0
     f = sf.StarForest(comm)
+    t0 = time.perf_counter()
     f.set_graph_spec(spec)
+    set_graph_s = time.perf_counter() - t0
     t0 = time.perf_counter()
     f.setup()
     setup_s = time.perf_counter() - t0
+    # The same forest planned on the device: the graph arrays
+    # are uploaded first (not timed), then set_graph_device + setup are timed.
+    dsetup = None
+    if not args.no_device_setup:
+        dev = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+        loc = dev(spec.local) if spec.local is not None else None
+        rr, ro = dev(spec.remote_rank), dev(spec.remote_off)
+        # one tiny device SetUp first: loads the planner's kernels (lazy module loading)
+        fw = sf.StarForest(comm)
+        fw.set_graph_device(1, 1, None, torch.tensor([rank], dtype=torch.int32, device="cuda"),
+                            torch.zeros(1, dtype=torch.int64, device="cuda"))
+        fw.setup()
+        del fw
+        runs = []
+        for _ in range(2):  # first: the planner's memory pool grows; second: steady state
+            fd = sf.StarForest(comm)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fd.set_graph_device(spec.nroots, spec.nleaves, loc, rr, ro)
+            t1 = time.perf_counter()
+            fd.setup()
+            t2 = time.perf_counter()
+            same = all(fd.group_plans(w) == f.group_plans(w) for w in (0, 1))
+            runs.append({"set_graph_s": allreduce(t1 - t0, "max"), "setup_s": allreduce(t2 - t1, "max"),
+                         "plan_equal": bool(allreduce(0.0 if same else 1.0, "sum") == 0.0)})
+            del fd
+        dsetup = {"first": runs[0], "steady": runs[1],
+                  "note": "same forest from device arrays; max over ranks; first = the planner's "
+                          "memory pool grows, steady = second SetUp in the process"}
+        del loc, rr, ro
     del spec
 
     unit = sf.Unit(sf.Kind.float64)
@@ -463,7 +496,8 @@ def ours(args, rank, world, local):
                        "parallelism": f"sf{world}", "us_per_op": ms_max * 1e3 / 2,
                        "bytes_per_step": bytes_all, "nvlink_bytes_per_step": net_bytes,
                        "l2": "inputs > L2: 1.07 GB roots + 1.09 GB leaves per rank at N=1",
-                       "setup_s": setup_s, "graph_gen_s": gen_s, "deterministic": True,
+                       "setup_s": setup_s, "set_graph_s": set_graph_s, "device_setup": dsetup,
+                       "graph_gen_s": gen_s, "deterministic": True,
                        "transport": args.transport if world > 1 else "none (self edges only)"},
             "gpu_launches": int(kl),
             "roofline": {"bound": "hbm", "kernel": dom_tag, "achieved": achieved, "peak": peak,

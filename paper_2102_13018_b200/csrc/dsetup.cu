@@ -29,7 +29,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cstdint>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "sfg.hpp"
 
@@ -51,11 +54,36 @@ int grid_for(int64_t n) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(sms) * 8)));
 }
 
+// Planner buffers come from the device's stream-ordered pool, which keeps
+// freed memory mapped (release threshold = max): a 1 GB cudaMalloc/cudaFree
+// costs 4-16 ms / up to 0.6 s on B200 (scripts/malloc_probe.py), the pool
+// hands it back in microseconds once it has grown.
+void ensure_pool() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  SFG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+  cudaMemPool_t pool;
+  SFG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = UINT64_MAX;
+  SFG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  done.push_back(dev);
+}
+
 template <class T>
 T* dalloc(int64_t n) {
   void* p = nullptr;
-  if (n > 0) SFG_CUDA(cudaMalloc(&p, static_cast<size_t>(n) * sizeof(T)));
+  if (n > 0) {
+    ensure_pool();
+    SFG_CUDA(cudaMallocAsync(&p, static_cast<size_t>(n) * sizeof(T), dstream()));
+  }
   return static_cast<T*>(p);
+}
+
+void dfree(void* p) {
+  if (p) cudaFreeAsync(p, dstream());
 }
 
 template <class T>
@@ -404,8 +432,8 @@ DevGraph::~DevGraph() {
   cudaDeviceSynchronize();
   int64_t* bufs[] = {local, off, ords, ridx != ords && ridx != local ? ridx : nullptr, loffs};
   for (int64_t* b : bufs)
-    if (b) cudaFree(b);
-  if (rank) cudaFree(rank);
+    if (b) dfree(b);
+  if (rank) dfree(rank);
 }
 
 void dev_narrow_index(const int64_t* src, int64_t n, int32_t* dst) {
@@ -428,7 +456,7 @@ bool dev_any_repeat(const std::vector<std::pair<const int64_t*, int64_t>>& lists
     if (n > 0) k_bitmap_distinct<<<grid_for(n), kT, 0, dstream()>>>(p, n, 0, bits, nullptr, sc.v);
   SFG_CUDA(cudaGetLastError());
   const bool rep = read1(sc.v) != 0;
-  SFG_CUDA(cudaFree(bits));
+  dfree(bits);
   return rep;
 }
 
@@ -464,17 +492,17 @@ void StarForest::set_graph_device(int64_t nroots, int64_t nleaves, const int64_t
       sort_keys(L, sorted, n);
       const int64_t lo = read1(sorted);
       if (lo < 0) {
-        cudaFree(sorted);
+        dfree(sorted);
         fail("set_graph: negative leaf index");
       }
       const int64_t dup = find_first(n, [=] __device__(int64_t i) { return i > 0 && sorted[i] == sorted[i - 1]; }, sc);
       if (dup < n) {
         const int64_t v = read1(sorted + dup);
-        cudaFree(sorted);
+        dfree(sorted);
         fail("set_graph: duplicate leaf index " + std::to_string(v) + " violates the forest property");
       }
       bound = read1(sorted + n - 1) + 1;
-      SFG_CUDA(cudaFree(sorted));
+      dfree(sorted);
     }
   } else if (leaf_local != nullptr) {
     bound = 0;
@@ -549,8 +577,8 @@ void StarForest::setup_device() {
     k_iota<<<gs, kT, 0, dstream()>>>(iota, n);
     sort_pairs(g.local, keys, iota, ord, n, 64);
     SFG_CUDA(cudaStreamSynchronize(dstream()));
-    cudaFree(iota);
-    cudaFree(keys);
+    dfree(iota);
+    dfree(keys);
   }
   std::vector<int64_t> start(static_cast<size_t>(P) + 1, 0), cnt(static_cast<size_t>(P), 0);
   if (P == 1 || n == 0) {
@@ -582,10 +610,10 @@ void StarForest::setup_device() {
     SFG_CUDA(cudaMemcpyAsync(host_first.data(), first, static_cast<size_t>(P) * 8, cudaMemcpyDeviceToHost,
                              dstream()));
     SFG_CUDA(cudaStreamSynchronize(dstream()));
-    cudaFree(first);
-    cudaFree(kin);
-    cudaFree(kout);
-    cudaFree(vin);
+    dfree(first);
+    dfree(kin);
+    dfree(kout);
+    dfree(vin);
     int64_t next = n;
     for (int r = P - 1; r >= 0; --r) {
       if (host_first[static_cast<size_t>(r)] < 0) continue;
@@ -649,7 +677,7 @@ void StarForest::setup_device() {
       at += lcnt[static_cast<size_t>(r)];
     }
     SFG_CUDA(cudaStreamSynchronize(dstream()));
-    cudaFree(payload);
+    dfree(payload);
   }
   recv.clear();
   mark("receive");
@@ -761,7 +789,7 @@ void dev_build_csr(DevPlan& d, int32_t* key, int32_t* val, int64_t total, int64_
     SFG_CUDA(cudaFreeAsync(t, dstream()));
     nq = read1(nruns);
   }
-  cudaFree(skey);
+  dfree(skey);
   // offs: exclusive sum over nq + 1 counts (the extra one set to 0 -> total)
   int32_t* offs = dalloc<int32_t>(nq + 1);
   SFG_CUDA(cudaMemsetAsync(cnts + nq, 0, sizeof(int32_t), dstream()));
@@ -830,7 +858,7 @@ void dev_build_csr(DevPlan& d, int32_t* key, int32_t* val, int64_t total, int64_
   SFG_CUDA(cudaGetLastError());
   d.ccsr_entries += static_cast<int64_t>(read1(sc.v));
   for (int32_t* b : {ent, roots, cnts, offs, split, ptab, flag, rcnt, fpos, rpos})
-    if (b) cudaFree(b);
+    if (b) dfree(b);
   if (tiled) {
     d.csr_np_max = static_cast<int32_t>(np_max);
     d.csr_piece_leaves = kPiece;

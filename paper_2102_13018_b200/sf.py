@@ -451,6 +451,18 @@ class StarForest:
             out.append(Group(rank.value, items, Pattern._from(pat)))
         return out
 
+    def group_plans(self, which: int) -> list[tuple[int, int, Pattern]]:
+        """(rank, count, pattern) per group without copying the item lists
+        (which = 0 root groups, 1 leaf groups)."""
+        i = self._info()
+        n = i.n_root_groups if which == 0 else i.n_leaf_groups
+        out = []
+        for g in range(n):
+            rank, cnt, pat = C.c_int(), C.c_int64(), L.sfg_pattern()
+            _check(_lib().sfg_sf_group(self._h, which, g, C.byref(rank), C.byref(cnt), C.byref(pat)))
+            out.append((rank.value, cnt.value, Pattern._from(pat)))
+        return out
+
     def root_groups(self) -> list[Group]:
         """Per root-owning rank: leaf ordinals + leaf-index pattern (starforest.hpp:114-118)."""
         return self._groups(0)
