@@ -436,6 +436,9 @@ DevGraph::~DevGraph() {
   if (rank) dfree(rank);
 }
 
+void* dev_pool_alloc(size_t bytes) { return dalloc<char>(static_cast<int64_t>(bytes)); }
+void dev_pool_free(void* p) { dfree(p); }
+
 void dev_narrow_index(const int64_t* src, int64_t n, int32_t* dst) {
   if (n <= 0) return;
   Scratch sc;

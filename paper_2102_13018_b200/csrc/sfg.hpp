@@ -550,6 +550,9 @@ void scatter_end(OpHandle& h);
 DPat to_dpat(const Pattern& p, const int32_t* dev_idx);
 
 // Device SetUp helpers (dsetup.cu), on the current device, synchronous.
+// Planner scratch from the stream-ordered pool (ordered on cudaStreamPerThread).
+void* dev_pool_alloc(size_t bytes);
+void dev_pool_free(void* p);
 // dst[i] = src[i] as int32; throws when a value exceeds the int32 range.
 void dev_narrow_index(const int64_t* src, int64_t n, int32_t* dst);
 // CSR build (StarForest::ensure_csr): keys/vals to int32 pairs (vals ==

@@ -523,8 +523,8 @@ void StarForest::ensure_csr() {
   const int64_t n_self = self ? leaf_groups_.front().count() : 0;
   int32_t *key = nullptr, *val = nullptr;
   if (total) {
-    SFG_CUDA(cudaMalloc(&key, static_cast<size_t>(total) * 4));
-    SFG_CUDA(cudaMalloc(&val, static_cast<size_t>(total) * 4));
+    key = static_cast<int32_t*>(dev_pool_alloc(static_cast<size_t>(total) * 4));
+    val = static_cast<int32_t*>(dev_pool_alloc(static_cast<size_t>(total) * 4));
   }
   const bool on_device = dg_ && !dg_->host_ready;
   int64_t at = 0;
@@ -551,15 +551,18 @@ void StarForest::ensure_csr() {
       });
       SFG_REQUIRE(!wide, "leaf index exceeds the int32 range of device plans");
       if (m) {
-        SFG_CUDA(cudaMemcpy(key + at, hk.data(), static_cast<size_t>(m) * 4, cudaMemcpyHostToDevice));
-        SFG_CUDA(cudaMemcpy(val + at, hv.data(), static_cast<size_t>(m) * 4, cudaMemcpyHostToDevice));
+        SFG_CUDA(cudaMemcpyAsync(key + at, hk.data(), static_cast<size_t>(m) * 4, cudaMemcpyHostToDevice,
+                                 cudaStreamPerThread));
+        SFG_CUDA(cudaMemcpyAsync(val + at, hv.data(), static_cast<size_t>(m) * 4, cudaMemcpyHostToDevice,
+                                 cudaStreamPerThread));
+        SFG_CUDA(cudaStreamSynchronize(cudaStreamPerThread));  // hk/hv go out of scope
       }
     }
     at += m;
   }
   dev_build_csr(d, key, val, total, n_self, nroots_, leaf_bound_, self);
-  if (key) cudaFree(key);
-  if (val) cudaFree(val);
+  dev_pool_free(key);
+  dev_pool_free(val);
   d.csr_built = true;
   pt.mark("csr build");
 }
