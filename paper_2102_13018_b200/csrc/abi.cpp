@@ -219,6 +219,10 @@ sfg_comm make_comm(sfg_world world, int nranks, int rank, int device, const sfg:
   else {
     SFG_REQUIRE(c.nccl_ != nullptr, "nranks > 1 without a world needs the nccl backend or control-plane callbacks");
     c.ctrl_ = sfg::make_nccl_ctrl(c.nccl_, rank, nranks, device);
+    // NCCL connects each peer pair on its first send/recv (~3 s on B200 for
+    // the first exchange): connect every pair here, at communicator
+    // creation, rather than inside the first SetUp.
+    c.ctrl_->alltoallv(std::vector<std::vector<uint8_t>>(static_cast<size_t>(nranks), std::vector<uint8_t>(8, 0)));
   }
   if (device >= 0 && cc.backend != "p2p") {
     if (cc.backend == "nccl")
