@@ -54,3 +54,17 @@ def test_error_reporting_without_gpu():
         assert "requires a graph-set star forest" in str(e)
     else:
         raise AssertionError("setup on a created forest must fail")
+
+
+def test_set_graph_device_needs_a_device_communicator():
+    """The device planner (dsetup.cu) refuses host-only communicators with the
+    reference's error mechanism (status + message), before touching memory."""
+    from paper_2102_13018_b200 import sf
+
+    c = sf.Comm(1, 0, -1)
+    f = sf.StarForest(c)
+    lib = _lib.load()
+    assert lib.sfg_sf_set_graph_device(f._h, 0, 0, None, None, None) != 0
+    assert b"needs a communicator with a device" in lib.sfg_last_error()
+    assert lib.sfg_sf_set_graph_device(f._h, -1, 0, None, None, None) != 0
+    assert b"negative root or leaf count" in lib.sfg_last_error()
