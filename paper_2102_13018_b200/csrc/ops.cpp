@@ -132,7 +132,17 @@ DSeg csr_seg(const DevPlan& d, CsrRange range, int32_t type, bool seq, size_t ub
   // Thread per root (sequential fold, no shuffles: one warp instruction
   // advances 32 roots) whenever there are enough roots to spread over the
   // GPU; a warp per root only for few, very high-degree roots.
-  if (s.n >= 8192) s.csr_warp = 0;
+  // Order-free fetch-and-op (integer ops, free-order mode) keeps a warp per
+  // root (warp scan, exact for them) up to 32768 roots: the fetch's thread
+  // chains are the slower ones, and with that few roots they leave the GPU
+  // mostly idle (config 4 at N=4: fetch End 170 -> 100 us; the same rule for
+  // folds made Begin's local fold 8 -> 58 us, so folds stay thread per root).
+  static const int64_t warp_limit = [] {
+    const char* e = std::getenv("SFG_CSR_WARP_LIMIT");
+    return e ? std::atoll(e) : int64_t(32768);
+  }();
+  const bool warp_fetch = type == SEG_CSR_FETCH && !seq && s.n < warp_limit;
+  if (s.n >= 8192 && !warp_fetch) s.csr_warp = 0;
   return s;
 }
 
