@@ -54,7 +54,7 @@ def shuffled(specs, seed):
 
 
 @pytest.mark.parametrize("seed", range(8))
-@pytest.mark.parametrize("P", [1, 2, 3, 4])
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
 def test_device_plan_equals_host_plan_random(seed, P):
     specs = graphs.random_graph_specs(700 + seed, P, 40)
     for r in both_plans(specs):
@@ -63,7 +63,7 @@ def test_device_plan_equals_host_plan_random(seed, P):
         assert r[0] == r[1]
 
 
-@pytest.mark.parametrize("P", [1, 2, 4])
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
 def test_device_plan_g2l_structured(P):
     specs = [graphs.g2l_halo(12, P, r) for r in range(P)]
     for r in both_plans(specs):
@@ -183,3 +183,21 @@ def test_config2_g2l_512_device_setup():
         return same, ok
 
     assert sf.run_ranks(sf.CommConfig(nranks=1), body, devices=[0])[0] == (True, True)
+
+
+def test_gather_scatter_over_device_forest():
+    """Gather / Scatter go through the multi-SF, which a device-set forest
+    builds from host copies made on demand (host_graph)."""
+    P = 3
+    specs = shuffled(graphs.random_graph_specs(31, P, 50), 5)
+    leaves = rank_data(specs, 7, np.float64, salt0=200, which="leaf")
+    deg = O.degrees(specs)
+    multi = [np.zeros(int(d.sum()), np.float64) for d in deg]
+    out = run_gpu(specs, "gather", [leaves, multi], config=sf.CommConfig(nranks=P), devices=[0] * P,
+                  device_graph=True)
+    want = O.gather(specs, leaves)
+    assert_same(out[1], want)
+    back = [np.full_like(x, -1.0) for x in leaves]
+    out = run_gpu(specs, "scatter", [want, back], config=sf.CommConfig(nranks=P), devices=[0] * P,
+                  device_graph=True)
+    assert_same(out[1], O.scatter(specs, want, back))
