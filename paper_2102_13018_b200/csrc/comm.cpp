@@ -218,6 +218,22 @@ class NcclCtrl final : public ControlPlane {
     if (dr) cudaFree(dr);
     return out;
   }
+  bool alltoallv_device(const uint8_t* send, const std::vector<int64_t>& soff,
+                        const std::vector<int64_t>& sbytes, uint8_t* recv, const std::vector<int64_t>& roff,
+                        const std::vector<int64_t>& rbytes) override {
+    SFG_CUDA(cudaSetDevice(dev_));
+    SFG_CUDA(cudaStreamSynchronize(cudaStreamPerThread));  // payload written on the caller's stream
+    SFG_NCCL(ncclGroupStart());
+    for (int r = 0; r < size_; ++r) {
+      if (r == rank_) continue;
+      const size_t i = static_cast<size_t>(r);
+      if (sbytes[i]) SFG_NCCL(ncclSend(send + soff[i], static_cast<size_t>(sbytes[i]), ncclUint8, r, c_, s_));
+      if (rbytes[i]) SFG_NCCL(ncclRecv(recv + roff[i], static_cast<size_t>(rbytes[i]), ncclUint8, r, c_, s_));
+    }
+    SFG_NCCL(ncclGroupEnd());
+    SFG_CUDA(cudaStreamSynchronize(s_));
+    return true;
+  }
   void barrier() override {
     uint8_t one = 1;
     std::vector<uint8_t> all(static_cast<size_t>(size_));

@@ -11,8 +11,9 @@
 //                               only when the indices are not increasing
 //   grouping by root rank       CUB stable radix sort on ceil(log2 P) key bits
 //   discovery payload           gather off[ords]; the self segment never
-//                               leaves HBM, remote segments cross the control
-//                               plane (halo-sized for partitioned grids)
+//                               leaves HBM, remote segments go device to device
+//                               over NCCL between processes (through the host
+//                               control plane otherwise)
 //   pattern classification      device find-first passes for contiguity and
 //                               the Affine3D inference + full verification;
 //                               distinct counts by bitmap or sorted uniques
@@ -638,51 +639,78 @@ void StarForest::setup_device() {
   int64_t* payload = dalloc<int64_t>(n);
   if (n) k_gather<<<gs, kT, 0, dstream()>>>(g.off, g.ords, payload, n);
   SFG_CUDA(cudaGetLastError());
-  std::vector<std::vector<uint8_t>> send(static_cast<size_t>(P));
-  for (int r = 0; r < P; ++r) {
-    if (r == me || cnt[static_cast<size_t>(r)] == 0) continue;
-    auto& b = send[static_cast<size_t>(r)];
-    b.resize(static_cast<size_t>(cnt[static_cast<size_t>(r)]) * 8);
-    SFG_CUDA(cudaMemcpyAsync(b.data(), payload + start[static_cast<size_t>(r)], b.size(),
-                             cudaMemcpyDeviceToHost, dstream()));
-  }
   SFG_CUDA(cudaStreamSynchronize(dstream()));
   mark("payload");
-  auto recv = P > 1 ? comm_->ctrl().alltoallv(std::move(send)) : std::vector<std::vector<uint8_t>>(1);
-  mark("discovery exchange");
 
-  // Leaf groups' items back to back: self first (never left HBM), then the
-  // received lists in ascending rank.
+  // Discovery exchange: the counts over the host control plane (8 bytes per
+  // peer), then the lists themselves device to device when the control
+  // plane can move device memory (NCCL between processes), else staged
+  // through the host. The self list never leaves HBM. Leaf groups' items are
+  // laid out back to back: self first, then the received lists in ascending
+  // rank.
   const int64_t nself = cnt[static_cast<size_t>(me)];
-  int64_t total = nself;
-  for (int r = 0; r < P; ++r)
-    if (r != me) {
-      SFG_REQUIRE(recv[static_cast<size_t>(r)].size() % 8 == 0, "malformed setup payload");
-      total += static_cast<int64_t>(recv[static_cast<size_t>(r)].size() / 8);
-    }
   std::vector<int64_t> lstart(static_cast<size_t>(P), 0), lcnt(static_cast<size_t>(P), 0);
   lcnt[static_cast<size_t>(me)] = nself;
   if (P == 1) {
     g.loffs = payload;
+    mark("discovery exchange");
   } else {
+    std::vector<std::vector<uint8_t>> csend(static_cast<size_t>(P));
+    for (int r = 0; r < P; ++r) {
+      if (r == me) continue;
+      csend[static_cast<size_t>(r)].resize(8);
+      std::memcpy(csend[static_cast<size_t>(r)].data(), &cnt[static_cast<size_t>(r)], 8);
+    }
+    auto crecv = comm_->ctrl().alltoallv(std::move(csend));
+    int64_t total = nself;
+    for (int r = 0; r < P; ++r) {
+      if (r == me) continue;
+      const auto& b = crecv[static_cast<size_t>(r)];
+      SFG_REQUIRE(b.size() == 8, "malformed setup payload");
+      std::memcpy(&lcnt[static_cast<size_t>(r)], b.data(), 8);
+      lstart[static_cast<size_t>(r)] = total;
+      total += lcnt[static_cast<size_t>(r)];
+    }
     g.loffs = dalloc<int64_t>(total);
     if (nself)
       SFG_CUDA(cudaMemcpyAsync(g.loffs, payload + start[static_cast<size_t>(me)], static_cast<size_t>(nself) * 8,
                                cudaMemcpyDeviceToDevice, dstream()));
-    int64_t at = nself;
+    std::vector<int64_t> soff(static_cast<size_t>(P)), sbytes(static_cast<size_t>(P)),
+        roff(static_cast<size_t>(P)), rbytes(static_cast<size_t>(P));
     for (int r = 0; r < P; ++r) {
-      if (r == me) continue;
-      const auto& b = recv[static_cast<size_t>(r)];
-      lstart[static_cast<size_t>(r)] = at;
-      lcnt[static_cast<size_t>(r)] = static_cast<int64_t>(b.size() / 8);
-      if (!b.empty())
-        SFG_CUDA(cudaMemcpyAsync(g.loffs + at, b.data(), b.size(), cudaMemcpyHostToDevice, dstream()));
-      at += lcnt[static_cast<size_t>(r)];
+      const size_t i = static_cast<size_t>(r);
+      soff[i] = start[i] * 8;
+      sbytes[i] = r == me ? 0 : cnt[i] * 8;
+      roff[i] = lstart[i] * 8;
+      rbytes[i] = r == me ? 0 : lcnt[i] * 8;
     }
     SFG_CUDA(cudaStreamSynchronize(dstream()));
+    const bool on_device = comm_->ctrl().alltoallv_device(reinterpret_cast<const uint8_t*>(payload), soff, sbytes,
+                                                          reinterpret_cast<uint8_t*>(g.loffs), roff, rbytes);
+    if (!on_device) {
+      std::vector<std::vector<uint8_t>> send(static_cast<size_t>(P));
+      for (int r = 0; r < P; ++r) {
+        const size_t i = static_cast<size_t>(r);
+        if (r == me || sbytes[i] == 0) continue;
+        send[i].resize(static_cast<size_t>(sbytes[i]));
+        SFG_CUDA(cudaMemcpyAsync(send[i].data(), payload + start[i], send[i].size(), cudaMemcpyDeviceToHost,
+                                 dstream()));
+      }
+      SFG_CUDA(cudaStreamSynchronize(dstream()));
+      auto recv = comm_->ctrl().alltoallv(std::move(send));
+      for (int r = 0; r < P; ++r) {
+        const size_t i = static_cast<size_t>(r);
+        if (r == me) continue;
+        SFG_REQUIRE(static_cast<int64_t>(recv[i].size()) == rbytes[i], "malformed setup payload");
+        if (rbytes[i])
+          SFG_CUDA(cudaMemcpyAsync(g.loffs + lstart[i], recv[i].data(), recv[i].size(), cudaMemcpyHostToDevice,
+                                   dstream()));
+      }
+      SFG_CUDA(cudaStreamSynchronize(dstream()));
+    }
+    mark(on_device ? "discovery exchange (device)" : "discovery exchange (host)");
     dfree(payload);
   }
-  recv.clear();
   mark("receive");
 
   // Groups in ascending rank, offsets validated (starforest.cpp:116-123),

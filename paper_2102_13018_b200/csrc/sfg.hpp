@@ -177,6 +177,17 @@ class ControlPlane {
   virtual void allgather(const void* in, size_t bytes, void* out) = 0;
   // send[r] goes to rank r; returns what each rank sent to me.
   virtual std::vector<std::vector<uint8_t>> alltoallv(std::vector<std::vector<uint8_t>> send) = 0;
+  // Same exchange between DEVICE buffers of the calling rank's GPU (the
+  // device SetUp's discovery payload): send + soff[r] holds sbytes[r] for
+  // rank r, rank r's payload lands at recv + roff[r] (rbytes[r], agreed
+  // beforehand). Entries for the own rank are ignored. Synchronous. Returns
+  // false when this control plane cannot move device memory (the caller then
+  // stages through the host).
+  virtual bool alltoallv_device(const uint8_t* send, const std::vector<int64_t>& soff,
+                                const std::vector<int64_t>& sbytes, uint8_t* recv,
+                                const std::vector<int64_t>& roff, const std::vector<int64_t>& rbytes) {
+    return false;
+  }
   virtual void barrier() = 0;
 };
 
