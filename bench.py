@@ -365,8 +365,8 @@ def ours(args, rank, world, local):
         sampler = ClockSampler(uuid if uuid.startswith("GPU-") else f"GPU-{uuid}")
         sampler.start()
         sampler.wait_first()
+    # Timed region: K steps, no per-launch instrumentation inside it.
     c0 = sf.counters()
-    sf.timing_enable(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     barrier()
@@ -379,10 +379,18 @@ def ours(args, rank, world, local):
     torch.cuda.synchronize()
     t_end = time.perf_counter()
     barrier()
-    sf.timing_enable(False)
     clocks = sampler.stop((t_start, t_end)) if sampler else None
     c1 = sf.counters()
+    # Per-launch CUDA events (kernel durations, bytes, NVLink bytes for the
+    # roofline) over a second pass of the same steps.
+    sf.timing_enable(True)
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            step()
+    torch.cuda.synchronize()
+    sf.timing_enable(False)
     timing = sf.timing_collect()
+    barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
     ms_max = allreduce(ms, "max")
     launches = sum(v["launches"] for v in timing.values())
