@@ -52,6 +52,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-device-setup", action="store_true")
+    p.add_argument("--graph", action="store_true",
+                   help="timed steps replay one CUDA graph of a step (captured after warm-up)")
     p.add_argument("--dims", type=lambda v: tuple(int(x) for x in v.split(",")), default=None,
                    help="process grid px,py,pz (default: 1x1x2 / 1x2x2 / 2x2x2 for 2 / 4 / 8 GPUs)")
     p.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
@@ -365,6 +367,21 @@ def ours(args, rank, world, local):
         sampler = ClockSampler(uuid if uuid.startswith("GPU-") else f"GPU-{uuid}")
         sampler.start()
         sampler.wait_first()
+    timed_step = step
+    graph_launches = None
+    if args.graph:
+        graph = torch.cuda.CUDAGraph()
+        g0 = sf.counters()["kernel_launches"]
+        with torch.cuda.graph(graph, stream=stream):
+            step()
+        graph_launches = sf.counters()["kernel_launches"] - g0  # kernel nodes per replayed step
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                graph.replay()
+        torch.cuda.synchronize()
+        barrier()
+        timed_step = graph.replay
+
     # Timed region: K steps, no per-launch instrumentation inside it.
     c0 = sf.counters()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -374,7 +391,7 @@ def ours(args, rank, world, local):
     with torch.cuda.stream(stream):
         ev0.record(stream)
         for _ in range(args.steps):
-            step()
+            timed_step()
         ev1.record(stream)
     torch.cuda.synchronize()
     t_end = time.perf_counter()
@@ -397,7 +414,8 @@ def ours(args, rank, world, local):
     bytes_step = sum(v["bytes"] for v in timing.values()) / args.steps
     bytes_all = allreduce(bytes_step, "sum")
     value = bytes_all / (ms_max * 1e-3) / 1e9
-    kl = allreduce(float(c1["kernel_launches"] - c0["kernel_launches"]), "sum")
+    kl = allreduce(float(c1["kernel_launches"] - c0["kernel_launches"] if graph_launches is None
+                         else graph_launches * args.steps), "sum")
     net_bytes = allreduce(float(c1["bytes_sent"] - c0["bytes_sent"]) / args.steps, "sum")
 
     # roofline of the dominant kernel (largest device time in the region)
@@ -502,6 +520,7 @@ def ours(args, rank, world, local):
                                    "Bcast REPLACE + Reduce SUM)",
                        "grid": [args.N] * 3, "decomposition": [px, py, pz],
                        "parallelism": f"sf{world}", "us_per_op": ms_max * 1e3 / 2,
+                       "launch": "CUDA graph replay per step" if args.graph else "eager API calls per step",
                        "bytes_per_step": bytes_all, "nvlink_bytes_per_step": net_bytes,
                        "l2": "inputs > L2: 1.07 GB roots + 1.09 GB leaves per rank at N=1",
                        "setup_s": setup_s, "set_graph_s": set_graph_s, "device_setup": dsetup,
