@@ -12,7 +12,8 @@
 // are zero-copy sends) — while the local (self-edge) scatter runs on the
 // caller's stream (or joins the pack launch when small). Per End: ONE unpack
 // launch (on the comm stream when it cannot conflict with the local scatter:
-// Bcast always, Reduce for the "coupled" roots), then the caller's stream
+// Reduce's fold of the "coupled" roots), then the caller's stream joins; a
+// p2p Bcast's unpack is already part of the put launch, so its End only
 // joins. Nothing synchronises the host with the GPU (§V
 // "stream-aware, sync-free").
 //
@@ -24,10 +25,10 @@
 // reference in both modes (free-order mode keeps an atomics path behind
 // SFG_FREE_ORDER_ATOMICS, pack.cpp:47-58 "atomics" mode).
 #include <algorithm>
-#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 
 #include "sfg.hpp"
 
