@@ -49,6 +49,9 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=8)
     p.add_argument("--sample-nz", type=int, default=64, help="reference sample: z planes per rank")
     p.add_argument("--sample-steps", type=int, default=10)
+    p.add_argument("--ref-threads", type=int, default=0,
+                   help="reference arm: rank threads (the reference parallelises by ranks only); "
+                        "0 = every host core (max 32), at least one per GPU")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-device-setup", action="store_true")
@@ -166,7 +169,11 @@ def reference_arm(args, rank, world):
     from oracle import ref
     from paper_2102_13018_b200 import graphs
 
-    P = world
+    # The reference is single-threaded per rank; its only host parallelism is
+    # more rank threads (run_ranks, threads backend). Use every host core: the
+    # sample grid is decomposed over P rank threads, sample_nz planes each.
+    cores = os.cpu_count() or 1
+    P = args.ref_threads if args.ref_threads > 0 else max(world, min(cores, 32))
     sample = (args.N, args.N, min(args.N, args.sample_nz * P))
     line = {"impl": "reference", "metric": METRIC, "unit": "GB/s", "higher_is_better": True,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup}
@@ -180,7 +187,6 @@ def reference_arm(args, rank, world):
     t = ref.time_bcast_reduce(specs, steps, 1)
     byts = sum(g2l_step_bytes(g) for g in geo)
     gbs = byts / (t["us_per_step"] * 1e-6) / 1e9
-    cores = os.cpu_count()
     line.update({
         "value": gbs, "ms_per_step": t["us_per_step"] / 1e3,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
