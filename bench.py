@@ -172,7 +172,7 @@ def reference_arm(args, rank, world):
     # The reference is single-threaded per rank; its only host parallelism is
     # more rank threads (run_ranks, threads backend). Use every host core: the
     # sample grid is decomposed over P rank threads, sample_nz planes each.
-    cores = os.cpu_count() or 1
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     P = args.ref_threads if args.ref_threads > 0 else max(world, min(cores, 32))
     sample = (args.N, args.N, min(args.N, args.sample_nz * P))
     line = {"impl": "reference", "metric": METRIC, "unit": "GB/s", "higher_is_better": True,
