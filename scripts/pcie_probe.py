@@ -1,12 +1,16 @@
 """PCIe bound of bench.py's e2e leg: 1 GiB pinned host <-> device copies,
 H2D alone, D2H alone, and both at once on two streams (what the pipelined
-e2e loop does every step). Prints one JSON line."""
+e2e loop does every step). Prints one JSON line. Under torchrun every rank
+probes its own GPU at the same time (the host-side aggregate bound)."""
 import json
+import os
 
 import torch
 
 
 def main(nbytes=1 << 30, reps=5):
+    rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(rank)
     n = nbytes // 8
     h_in = torch.empty(n, dtype=torch.float64).pin_memory()
     h_out = torch.empty(n, dtype=torch.float64).pin_memory()
@@ -44,7 +48,7 @@ def main(nbytes=1 << 30, reps=5):
     d2h = timed(lambda: h_out.copy_(d_b, non_blocking=True))
     bi = timed(both)
     gb = nbytes / 1e9
-    print(json.dumps({"bytes": nbytes, "h2d_ms": h2d, "h2d_GBps": gb / (h2d * 1e-3),
+    print(json.dumps({"gpu": rank, "world": int(os.environ.get("WORLD_SIZE", "1")), "bytes": nbytes, "h2d_ms": h2d, "h2d_GBps": gb / (h2d * 1e-3),
                       "d2h_ms": d2h, "d2h_GBps": gb / (d2h * 1e-3),
                       "bidir_ms": bi, "bidir_GBps_per_direction": gb / (bi * 1e-3)}))
 
