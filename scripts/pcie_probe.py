@@ -10,7 +10,12 @@ import torch
 
 def main(nbytes=1 << 30, reps=5):
     rank = int(os.environ.get("LOCAL_RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     torch.cuda.set_device(rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    sync = (lambda: torch.distributed.barrier()) if world > 1 else (lambda: None)
     n = nbytes // 8
     h_in = torch.empty(n, dtype=torch.float64).pin_memory()
     h_out = torch.empty(n, dtype=torch.float64).pin_memory()
@@ -25,6 +30,7 @@ def main(nbytes=1 << 30, reps=5):
         best = None
         for _ in range(reps):
             torch.cuda.synchronize()
+            sync()  # every rank's copies start together
             e0.record()
             fn()
             e1.record()
@@ -47,8 +53,10 @@ def main(nbytes=1 << 30, reps=5):
     h2d = timed(lambda: d_a.copy_(h_in, non_blocking=True))
     d2h = timed(lambda: h_out.copy_(d_b, non_blocking=True))
     bi = timed(both)
+    if world > 1:
+        torch.distributed.destroy_process_group()
     gb = nbytes / 1e9
-    print(json.dumps({"gpu": rank, "world": int(os.environ.get("WORLD_SIZE", "1")), "bytes": nbytes, "h2d_ms": h2d, "h2d_GBps": gb / (h2d * 1e-3),
+    print(json.dumps({"gpu": rank, "world": world, "bytes": nbytes, "h2d_ms": h2d, "h2d_GBps": gb / (h2d * 1e-3),
                       "d2h_ms": d2h, "d2h_GBps": gb / (d2h * 1e-3),
                       "bidir_ms": bi, "bidir_GBps_per_direction": gb / (bi * 1e-3)}))
 
