@@ -508,8 +508,26 @@ def ours(args, rank, world, local):
         e2e = {"value": bytes_all / (ems * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ems,
                "h2d_bytes_per_step": int(hb), "d2h_bytes_per_step": int(hb),
                "pipelined": "3 root buffers: H2D, SF work and D2H of consecutive steps overlap"}
-        if world == 1:  # every interior leaf is a copy of its root: Reduce SUM doubles it
-            e2e["result_ok"] = bool(torch.equal(host_out, host_in * 2))
+        # every step starts from host_in: Reduce SUM folds each root with its
+        # interior copy and one copy per neighbour ghosting it (any N)
+        want = graphs.g2l_reduce_expect(geo, host_in.cuda()).cpu()
+        ok = float(torch.equal(host_out, want))
+        e2e["result_ok"] = bool(allreduce(ok, "sum") == world)
+        del want
+
+    # Result check at full size on every rank, any N (after the timed work):
+    # roots = their local ids, one Bcast REPLACE + Reduce SUM, closed form.
+    ids = torch.arange(geo.n_owned, dtype=torch.float64, device="cuda")
+    leaf.fill_(-1.0)
+    with torch.cuda.stream(stream):
+        step_on(ids)
+    torch.cuda.synchronize()
+    chk = graphs.g2l_check(geo, leaf, ids)
+    del ids
+    nbad = allreduce(0.0 if (chk["leaf_ok"] and chk["root_ok"]) else 1.0, "sum")
+    check = {"result_ok": nbad == 0, "ranks_failed": int(nbad),
+             "what": "roots = local ids; Bcast REPLACE + Reduce SUM; every leaf of the ghosted box "
+                     "and every root equal their closed form (id, neighbour's id, id*(2+ghost copies))"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -544,6 +562,8 @@ def ours(args, rank, world, local):
                             "GBps": v["bytes"] / (v["total_ms"] * 1e-3) / 1e9 if v["total_ms"] else None}
                         for k, v in timing.items()},
             "nvlink": nvlink,
+            "check": check,
+            "result_ok": check["result_ok"],
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,

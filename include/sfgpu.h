@@ -140,8 +140,20 @@ int sfg_sf_set_graph(sfg_sf sf, int64_t nroots, int64_t nleaves, const int64_t* 
  * (group lists stay in HBM, host copies are made only when asked for). */
 int sfg_sf_set_graph_device(sfg_sf sf, int64_t nroots, int64_t nleaves, const int64_t* leaf_local,
                             const int32_t* remote_rank, const int64_t* remote_off);
-/* StarForest::setup (starforest.hpp:79; starforest.cpp:82-161). Collective. */
+/* StarForest::setup (starforest.hpp:79; starforest.cpp:82-161). Collective.
+ * On a device communicator SetUp also builds the device plan, the
+ * root-sorted fold plan (when a root has several leaves) and one staging slot
+ * for 8-byte units, so no later Begin/End of an 8-byte unit allocates device
+ * memory or synchronises the host. */
 int sfg_sf_setup(sfg_sf sf, int alg);
+/* The same for another unit (kind, blocklen): call before capturing a first
+ * operation of that unit into a CUDA graph (Begin inside a capture fails
+ * with a message naming this call otherwise). Collective on p2p.
+ * Replays of a captured operation must be stream-ordered after eager
+ * operations issued earlier on the same forest (they share its staging
+ * slots and device message counters). No reference equivalent (the
+ * reference has no device state). */
+int sfg_sf_prepare(sfg_sf sf, int kind, int64_t blocklen);
 int sfg_sf_get_info(sfg_sf sf, sfg_sf_info* out);
 /* two_sided() groups: which = 0 root_ranks (items = leaf ordinals),
  * which = 1 leaf_ranks (items = root offsets) — starforest.hpp:47-55. */
@@ -202,7 +214,9 @@ int sfg_spmv(sfg_sf ghost_sf, sfg_mat diag, sfg_mat offdiag, const void* x_owned
 int sfg_spmv_transpose(sfg_sf ghost_sf, sfg_mat diag, sfg_mat offdiag, const void* x_owned,
                        void* lvec, void* y, void* stream);
 
-/* Handle introspection (OpHandle::kind/op/ended, ops.hpp:38-45) and release. */
+/* Handle introspection (OpHandle::kind/op/ended, ops.hpp:38-45) and release.
+ * Freeing a handle that was begun but never ended fails on the p2p backend
+ * (the staging slot is retired, the handle is still freed). */
 int sfg_handle_info(sfg_handle h, int* opkind, int* op, int* ended);
 int sfg_handle_free(sfg_handle h);
 

@@ -189,6 +189,11 @@ class StarForest {
     detail::check(sfg_sf_set_graph_device(h_, nroots, nleaves, leaf_local, remote_rank, remote_off));
   }
   void setup(SetupAlg alg = SetupAlg::automatic) { detail::check(sfg_sf_setup(h_, static_cast<int>(alg))); }
+  // Device plans and a staging slot for `unit` before a CUDA-graph capture
+  // (SetUp already did this for 8-byte units). Collective on p2p.
+  void prepare(const Unit& unit) {
+    detail::check(sfg_sf_prepare(h_, static_cast<int>(unit.kind), unit.blocklen));
+  }
 
   SfState state() const { return static_cast<SfState>(info().state); }
   std::int64_t nroots() const { return info().nroots; }

@@ -94,6 +94,20 @@ def bcast(specs, rootdata, leafdata, op="replace", blocklen=1):
     return leaves
 
 
+def bcast_edges(edge_arrays, rootdata, leafdata, op="replace", blocklen=1):
+    """oracle::bcast over an arbitrary edge list (rr, ro, lr, li) — e.g. a
+    transposed graph where a leaf may have several roots (selfcheck.cpp:
+    165-197 duality: GlobalGraph::transposed)."""
+    rr, ro, lr, li = (np.ascontiguousarray(a) for a in edge_arrays)
+    rr, lr = rr.astype(np.int32), lr.astype(np.int32)
+    ro, li = ro.astype(np.int64), li.astype(np.int64)
+    roots, leaves = _copy(rootdata), _copy(leafdata)
+    k = _kind(roots, blocklen)
+    _load().oracle_bcast(rr.size, rr.ctypes.data, ro.ctypes.data, lr.ctypes.data, li.ctypes.data,
+                         k, blocklen, OPS[op], _ptrs(roots), _ptrs(leaves))
+    return leaves
+
+
 def reduce(specs, leafdata, rootdata, op="sum", blocklen=1):
     keep, e = _e(specs)
     leaves, roots = _copy(leafdata), _copy(rootdata)
@@ -143,43 +157,81 @@ def scatter(specs, multiroot, leafdata, blocklen=1):
 
 
 # ------------------------------------------------------------------ SpMV
+def _split(rowptr, colind, vals, starts, r):
+    """split_matrix (spmv.hpp:95-127) restated: the diagonal block's rows as
+    (local col, val) lists in stored order, the off-diagonal block's rows as
+    (reduced col, val) lists in ascending global column order (Csr::
+    from_triplets sorts each row by column, spmv.hpp:44-56), and garray."""
+    r0, r1 = int(starts[r]), int(starts[r + 1])
+    diag, off, ghost = [], [], set()
+    for row in range(r0, r1):
+        d, o = [], []
+        for i in range(int(rowptr[row]), int(rowptr[row + 1])):
+            c = int(colind[i])
+            if r0 <= c < r1:
+                d.append((c - r0, vals[i]))
+            else:
+                o.append((c, vals[i]))
+                ghost.add(c)
+        diag.append(sorted(d, key=lambda t: t[0]))
+        off.append(sorted(o, key=lambda t: t[0]))
+    garray = sorted(ghost)
+    pos = {g: k for k, g in enumerate(garray)}
+    off = [[(pos[c], v) for c, v in row] for row in off]
+    return diag, off, np.array(garray, np.int64)
+
+
 def spmv(glob, layout, x, transpose: bool = False):
     """The reference's distributed SpMV (spmv.hpp:149-169) restated
-    sequentially: split_matrix per rank, then the Csr loops in the reference
-    order (diag product, then += off-diagonal product; for the transpose
-    A^T x into zeros, B^T x into zeros, Reduce(SUM) into the owners in
-    ascending rank order, ops.cpp:364,372-376). Pure-Python loops: test-sized
-    matrices only. `glob` is a paper_2102_13018_b200.spmv.Csr."""
-    import numpy as np
-
-    from paper_2102_13018_b200 import spmv as S
-
-    P = layout.nranks()
-    ms = [S.split_matrix(glob, layout, layout, r) for r in range(P)]
+    sequentially from the global CSR (``glob.rowptr/colind/vals``) and the
+    row layout (``layout.starts``): per rank the diagonal product, then +=
+    the off-diagonal product over the gathered ghosts; for the transpose
+    A^T x and B^T x into zeros, then Reduce(SUM) of the ghost partial sums
+    into their owners in ascending rank order (ops.cpp:364,372-376).
+    Pure-Python loops: test-sized matrices only. Shares no code with the
+    product package."""
+    starts = np.asarray(layout.starts, np.int64)
+    P = len(starts) - 1
+    dt = np.asarray(glob.vals).dtype
+    parts = [_split(glob.rowptr, glob.colind, glob.vals, starts, r) for r in range(P)]
     ys = []
-    if not transpose:
-        for r, m in enumerate(ms):
-            xo = x[layout.begin(r):layout.end(r)]
-            y = m.diag.multiply(xo)
-            m.offdiag.multiply_add(x[m.garray], y)
-            ys.append(y)
-        return np.concatenate(ys)
-    lvecs = []
-    for r, m in enumerate(ms):
-        xo = x[layout.begin(r):layout.end(r)]
-        y = np.zeros(layout.local_size(r), dtype=glob.vals.dtype)
-        m.diag.multiply_transpose_add(xo, y)
-        lv = np.zeros(len(m.garray), dtype=glob.vals.dtype)
-        m.offdiag.multiply_transpose_add(xo, lv)
-        ys.append(y)
-        lvecs.append(lv)
     with np.errstate(over="ignore"):
+        if not transpose:
+            for r, (diag, off, garray) in enumerate(parts):
+                xo = x[starts[r]:starts[r + 1]]
+                xg = x[garray]
+                y = np.zeros(len(diag), dtype=dt)
+                for i, row in enumerate(diag):
+                    acc = dt.type(0)
+                    for c, v in row:
+                        acc = acc + v * xo[c]
+                    y[i] = acc
+                for i, row in enumerate(off):
+                    acc = dt.type(0)
+                    for c, v in row:
+                        acc = acc + v * xg[c]
+                    y[i] = y[i] + acc
+                ys.append(y)
+            return np.concatenate(ys)
+        lvecs = []
+        for r, (diag, off, garray) in enumerate(parts):
+            xo = x[starts[r]:starts[r + 1]]
+            y = np.zeros(len(diag), dtype=dt)
+            lv = np.zeros(len(garray), dtype=dt)
+            for i, row in enumerate(diag):
+                for c, v in row:
+                    y[c] = y[c] + v * xo[i]
+            for i, row in enumerate(off):
+                for c, v in row:
+                    lv[c] = lv[c] + v * xo[i]
+            ys.append(y)
+            lvecs.append(lv)
         for r in range(P):  # owners fold remote contributions rank by rank
             for s in range(P):
                 if s == r:
                     continue
-                g = ms[s].garray
-                mine = (g >= layout.begin(r)) & (g < layout.end(r))
-                for gi, v in zip(g[mine], lvecs[s][mine]):
-                    ys[r][gi - layout.begin(r)] = ys[r][gi - layout.begin(r)] + v
+                g = parts[s][2]
+                for gi, v in zip(g, lvecs[s]):
+                    if starts[r] <= gi < starts[r + 1]:
+                        ys[r][gi - starts[r]] = ys[r][gi - starts[r]] + v
     return np.concatenate(ys)

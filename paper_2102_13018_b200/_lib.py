@@ -94,6 +94,7 @@ _SIGS = {
     "sfg_sf_set_graph": (C.c_int, [_V, C.c_int64, C.c_int64, _V, _V, _V]),
     "sfg_sf_set_graph_device": (C.c_int, [_V, C.c_int64, C.c_int64, _V, _V, _V]),
     "sfg_sf_setup": (C.c_int, [_V, C.c_int]),
+    "sfg_sf_prepare": (C.c_int, [_V, C.c_int, C.c_int64]),
     "sfg_sf_get_info": (C.c_int, [_V, C.POINTER(sfg_sf_info)]),
     "sfg_sf_group": (C.c_int, [_V, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int64),
                                C.POINTER(sfg_pattern)]),

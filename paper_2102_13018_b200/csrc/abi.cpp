@@ -464,9 +464,25 @@ int sfg_handle_info(sfg_handle h, int* opkind, int* op, int* ended) {
 int sfg_handle_free(sfg_handle h) {
   return guard([&] {
     auto* x = reinterpret_cast<sfg::OpHandle*>(h);
-    if (x && x->stg && x->sf) x->sf->release_staging(x->stg, x->stream);
+    if (x && x->stg && x->sf) {
+      if (!x->ended && x->sf->comm().p2p() && x->stg->flags) {
+        // Begun, never ended: a peer's message may still be unconsumed in
+        // the slot and its device counters are one behind, so the slot is
+        // retired (never reused; freed with the forest), not returned.
+        x->stg->retired = true;
+        x->stg = nullptr;
+        delete x;
+        sfg::fail("operation freed without End on the p2p backend; its staging slot is retired "
+                  "(every rank must end every operation it began)");
+      }
+      x->sf->release_staging(x->stg, x->stream);
+    }
     delete x;
   });
+}
+
+int sfg_sf_prepare(sfg_sf sf, int kind, int64_t blocklen) {
+  return guard([&] { SF(sf)->prepare(unit(kind, blocklen).bytes()); });
 }
 
 int sfg_pattern_analyze(const int64_t* idx, int64_t n, int infer_affine, int64_t ex, int64_t exy,

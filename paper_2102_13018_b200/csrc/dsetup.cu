@@ -759,6 +759,7 @@ void StarForest::setup_device() {
   leaf_groups_ = std::move(leaves);
   g.host_ready = false;
   state_ = SfState::set_up;
+  prepare_default();
 }
 
 // Host copies of a device-set graph and its groups, for the host-side

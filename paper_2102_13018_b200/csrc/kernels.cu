@@ -99,72 +99,6 @@ __device__ __forceinline__ T apply_op(T a, T b) {
   }
 }
 
-// Atomic read-modify-write returning the previous value. Native atomics where
-// the hardware has them, a CAS loop with the reference comparison otherwise.
-template <class T, int OP>
-__device__ __forceinline__ T atomic_fetch_apply(T* p, T v) {
-  if constexpr (sizeof(T) < 4) {
-    __trap();
-    return v;
-  } else if constexpr (OP == OP_SUM && std::is_same_v<T, double>) {
-    return atomicAdd(p, v);
-  } else if constexpr (OP == OP_SUM && sizeof(T) == 8) {
-    return static_cast<T>(atomicAdd(reinterpret_cast<unsigned long long*>(p),
-                                    static_cast<unsigned long long>(v)));
-  } else if constexpr (OP == OP_SUM && sizeof(T) == 4) {
-    return static_cast<T>(
-        atomicAdd(reinterpret_cast<unsigned int*>(p), static_cast<unsigned int>(v)));
-  } else if constexpr (OP == OP_MAX && std::is_same_v<T, int64_t>) {
-    return static_cast<T>(atomicMax(reinterpret_cast<long long*>(p), static_cast<long long>(v)));
-  } else if constexpr (OP == OP_MIN && std::is_same_v<T, int64_t>) {
-    return static_cast<T>(atomicMin(reinterpret_cast<long long*>(p), static_cast<long long>(v)));
-  } else if constexpr (OP == OP_MAX && std::is_same_v<T, int32_t>) {
-    return atomicMax(p, v);
-  } else if constexpr (OP == OP_MIN && std::is_same_v<T, int32_t>) {
-    return atomicMin(p, v);
-  } else if constexpr (OP == OP_BAND && std::is_integral_v<T> && sizeof(T) == 8) {
-    return static_cast<T>(atomicAnd(reinterpret_cast<unsigned long long*>(p),
-                                    static_cast<unsigned long long>(v)));
-  } else if constexpr (OP == OP_BOR && std::is_integral_v<T> && sizeof(T) == 8) {
-    return static_cast<T>(atomicOr(reinterpret_cast<unsigned long long*>(p),
-                                   static_cast<unsigned long long>(v)));
-  } else if constexpr (OP == OP_BAND && std::is_integral_v<T> && sizeof(T) == 4) {
-    return static_cast<T>(
-        atomicAnd(reinterpret_cast<unsigned int*>(p), static_cast<unsigned int>(v)));
-  } else if constexpr (OP == OP_BOR && std::is_integral_v<T> && sizeof(T) == 4) {
-    return static_cast<T>(
-        atomicOr(reinterpret_cast<unsigned int*>(p), static_cast<unsigned int>(v)));
-  } else if constexpr (sizeof(T) == 8) {
-    auto* a = reinterpret_cast<unsigned long long*>(p);
-    unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(a);
-    unsigned long long assumed;
-    T cur;
-    do {
-      assumed = old;
-      cur = *reinterpret_cast<T*>(&assumed);
-      T nv = apply_op<T, OP>(cur, v);
-      unsigned long long nb = *reinterpret_cast<unsigned long long*>(&nv);
-      if (nb == assumed) return cur;
-      old = atomicCAS(a, assumed, nb);
-    } while (old != assumed);
-    return cur;
-  } else {
-    auto* a = reinterpret_cast<unsigned int*>(p);
-    unsigned int old = *reinterpret_cast<volatile unsigned int*>(a);
-    unsigned int assumed;
-    T cur;
-    do {
-      assumed = old;
-      cur = *reinterpret_cast<T*>(&assumed);
-      T nv = apply_op<T, OP>(cur, v);
-      unsigned int nb = *reinterpret_cast<unsigned int*>(&nv);
-      if (nb == assumed) return cur;
-      old = atomicCAS(a, assumed, nb);
-    } while (old != assumed);
-    return cur;
-  }
-}
-
 struct ItemMap {
   int64_t bl;
   bool small;
@@ -188,7 +122,7 @@ __device__ __forceinline__ bool skipped(const uint32_t* bits, int64_t v) {
 }
 
 // dst[dpat(i)] (op)= src[spat(i)] over this CTA's items.
-template <class T, int OP, bool ATOMIC>
+template <class T, int OP>
 __device__ __forceinline__ void run_pair(const DSeg& s, const LaunchParams& P, int64_t blk) {
   const T* __restrict__ src = static_cast<const T*>(P.bufs[s.src_buf]);
   T* dst = static_cast<T*>(P.bufs[s.dst_buf]);
@@ -212,7 +146,7 @@ __device__ __forceinline__ void run_pair(const DSeg& s, const LaunchParams& P, i
       }
       di[u] = dv * P.bl + k;
       v[u] = src[si];
-      if constexpr (OP != OP_REPLACE && !ATOMIC) d[u] = dst[di[u]];
+      if constexpr (OP != OP_REPLACE) d[u] = dst[di[u]];
     }
   }
 #pragma unroll
@@ -220,8 +154,6 @@ __device__ __forceinline__ void run_pair(const DSeg& s, const LaunchParams& P, i
     if (di[u] < 0) continue;
     if constexpr (OP == OP_REPLACE) {
       dst[di[u]] = v[u];
-    } else if constexpr (ATOMIC) {
-      (void)atomic_fetch_apply<T, OP>(dst + di[u], v[u]);
     } else {
       dst[di[u]] = apply_op<T, OP>(d[u], v[u]);
     }
@@ -233,7 +165,7 @@ __device__ __forceinline__ void run_pair(const DSeg& s, const LaunchParams& P, i
 // consecutive elements of the CTA's chunk; index maps are evaluated once per
 // run (not per element), then the lanes stream the run with kItems
 // independent loads in flight each.
-template <class T, int OP, bool ATOMIC>
+template <class T, int OP>
 __device__ __forceinline__ void run_pair_rows(const DSeg& s, const LaunchParams& P, int64_t blk) {
   const T* __restrict__ src = static_cast<const T*>(P.bufs[s.src_buf]);
   T* dst = static_cast<T*>(P.bufs[s.dst_buf]);
@@ -260,7 +192,7 @@ __device__ __forceinline__ void run_pair_rows(const DSeg& s, const LaunchParams&
       const int64_t i = lane + 32 * u;
       if (i < len) {
         v[u] = sp[i];
-        if constexpr (OP != OP_REPLACE && !ATOMIC) d[u] = dp[i];
+        if constexpr (OP != OP_REPLACE) d[u] = dp[i];
       }
     }
     // Coupled roots (skip_dst): one bitmap word per lane covers the whole run
@@ -296,8 +228,6 @@ __device__ __forceinline__ void run_pair_rows(const DSeg& s, const LaunchParams&
       if (keep) {
         if constexpr (OP == OP_REPLACE)
           dp[i] = v[u];
-        else if constexpr (ATOMIC)
-          (void)atomic_fetch_apply<T, OP>(dp + i, v[u]);
         else
           dp[i] = apply_op<T, OP>(d[u], v[u]);
       }
@@ -375,6 +305,30 @@ __device__ __forceinline__ void csr_piece(const DSeg& s, int64_t r, int q, int32
   hi = q == s.csr_np - 1 ? __ldg(s.csr_hi + r) : __ldg(pt + (q + 1) * s.csr_pt_step - 1);
 }
 
+// Group of a CSR entry under a free-order fetch shuffle (see FetchShuffle).
+__device__ __forceinline__ int shuf_group(const FetchShuffle& f, int32_t e) {
+  if (e >= 0) return 0;
+  const int32_t pos = -e - 1;
+  int k = 0;
+  const int nrem = f.n - f.self;
+  while (k + 1 < nrem && pos >= f.off[k + 1]) ++k;
+  return f.self + k;
+}
+
+// First entry in [lo, hi) whose group is >= g (groups ascend along a root's
+// entries).
+__device__ __forceinline__ int32_t shuf_bound(const FetchShuffle& f, const int32_t* ent, int32_t lo,
+                                              int32_t hi, int g) {
+  while (lo < hi) {
+    const int32_t mid = lo + (hi - lo) / 2;
+    if (shuf_group(f, __ldg(ent + mid)) < g)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
 // Root-sorted fold in the reference order (self leaves ascending, then remote
 // groups ascending rank, each in ascending leaf order), one thread per root
 // item: sequential per root, so floating-point results are bit-identical to
@@ -400,6 +354,17 @@ __device__ __forceinline__ void run_csr_t(const DSeg& s, const LaunchParams& P, 
     const int32_t hi = __ldg(s.csr_hi + r);
     if (lo >= hi) return;
     const int64_t ro = static_cast<int64_t>(__ldg(s.csr_roots + r)) * bl + k;
+    if (FETCH && P.shuf.n > 1) {
+      T acc = root[ro];
+      for (int q = 0; q < P.shuf.n; ++q) {
+        const int g = P.shuf.perm[q];
+        const int32_t a = shuf_bound(P.shuf, s.csr_ent, lo, hi, g);
+        const int32_t b = shuf_bound(P.shuf, s.csr_ent, a, hi, g + 1);
+        if (a < b) acc = csr_thread_range<T, OP, kB, FETCH>(s, leaf, stage, aux, bl, k, a, b, acc);
+      }
+      root[ro] = acc;
+      return;
+    }
     root[ro] = csr_thread_range<T, OP, kB, FETCH>(s, leaf, stage, aux, bl, k, lo, hi, root[ro]);
     return;
   }
@@ -528,6 +493,17 @@ __device__ __forceinline__ void run_csr_warp(const DSeg& s, const LaunchParams& 
     const int32_t hi = __ldg(s.csr_hi + r);
     if (lo >= hi) return;
     const int64_t ro = static_cast<int64_t>(__ldg(s.csr_roots + r)) * bl + k;
+    if (fetch && P.shuf.n > 1) {
+      T acc = root[ro];
+      for (int q = 0; q < P.shuf.n; ++q) {
+        const int g = P.shuf.perm[q];
+        const int32_t a = shuf_bound(P.shuf, s.csr_ent, lo, hi, g);
+        const int32_t b = shuf_bound(P.shuf, s.csr_ent, a, hi, g + 1);
+        if (a < b) acc = csr_warp_range<T, OP>(s, leaf, stage, aux, bl, k, a, b, acc, true);
+      }
+      if (lane == 0) root[ro] = acc;
+      return;
+    }
     const T acc = csr_warp_range<T, OP>(s, leaf, stage, aux, bl, k, lo, hi, root[ro], fetch);
     if (lane == 0) root[ro] = acc;
     return;
@@ -545,39 +521,6 @@ __device__ __forceinline__ void run_csr_warp(const DSeg& s, const LaunchParams& 
       const T acc = csr_warp_range<T, OP>(s, leaf, stage, aux, bl, k, lo, hi, root[ro], fetch);
       if (lane == 0) root[ro] = acc;
     }
-  }
-}
-
-// Free-order fetch-and-op: fetched = atomic(root[dpat(i)] op= src[spat(i)]),
-// written to aux[spat(i)] (leafupdate for self edges, the reply slot in place
-// for remote contributions).
-template <class T, int OP>
-__device__ __forceinline__ void run_atomic_fetch(const DSeg& s, const LaunchParams& P,
-                                                 int64_t blk) {
-  const T* src = static_cast<const T*>(P.bufs[s.src_buf]);
-  T* root = static_cast<T*>(P.bufs[s.dst_buf]);
-  T* aux = static_cast<T*>(P.bufs[s.aux_buf]);
-  const int64_t total = s.n * P.bl;
-  const ItemMap im{P.bl, total < (int64_t(1) << 31), P.bldiv};
-  const int64_t base = blk * (kThreads * kItems) + threadIdx.x;
-  T v[kItems];
-  int64_t si[kItems], di[kItems];
-#pragma unroll
-  for (int u = 0; u < kItems; ++u) {
-    const int64_t e = base + static_cast<int64_t>(u) * kThreads;
-    di[u] = -1;
-    if (e < total) {
-      int64_t i, k;
-      im.split(e, i, k);
-      si[u] = pat_index(s.src, i) * P.bl + k;
-      di[u] = pat_index(s.dst, i) * P.bl + k;
-      v[u] = src[si[u]];
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < kItems; ++u) {
-    if (di[u] < 0) continue;
-    aux[si[u]] = atomic_fetch_apply<T, OP>(root + di[u], v[u]);
   }
 }
 
@@ -678,22 +621,14 @@ __global__ void __launch_bounds__(kThreads, FULL ? 3 : 4) segments_kernel(const 
     case SEG_PAIR:
       if (seg.run > 0) {
         if (seg.replace)
-          run_pair_rows<T, OP_REPLACE, false>(seg, P, blk);
+          run_pair_rows<T, OP_REPLACE>(seg, P, blk);
         else
-          run_pair_rows<T, OP, false>(seg, P, blk);
+          run_pair_rows<T, OP>(seg, P, blk);
       } else {
         if (seg.replace)
-          run_pair<T, OP_REPLACE, false>(seg, P, blk);
+          run_pair<T, OP_REPLACE>(seg, P, blk);
         else
-          run_pair<T, OP, false>(seg, P, blk);
-      }
-      break;
-    case SEG_PAIR_ATOMIC:
-      if constexpr (OP != OP_REPLACE && sizeof(T) >= 4) {
-        if (seg.run > 0)
-          run_pair_rows<T, OP, true>(seg, P, blk);
-        else
-          run_pair<T, OP, true>(seg, P, blk);
+          run_pair<T, OP>(seg, P, blk);
       }
       break;
     case SEG_CSR_FOLD:
@@ -711,9 +646,6 @@ __global__ void __launch_bounds__(kThreads, FULL ? 3 : 4) segments_kernel(const 
         else
           run_csr<T, OP>(seg, P, blk, true);
       }
-      break;
-    case SEG_ATOMIC_FETCH:
-      if constexpr (OP != OP_REPLACE && sizeof(T) >= 4 && FULL) run_atomic_fetch<T, OP>(seg, P, blk);
       break;
     default:
       break;
@@ -738,7 +670,7 @@ template <class T, int OP>
 void launch_t(const LaunchParams& p, int64_t blocks, cudaStream_t st) {
   bool full = false;
   for (int s = 0; s < p.nseg; ++s)
-    full = full || (p.seg[s].type != SEG_PAIR && p.seg[s].type != SEG_PAIR_ATOMIC);
+    full = full || p.seg[s].type != SEG_PAIR;
   if constexpr (OP == OP_REPLACE) {
     segments_kernel<T, OP, false><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
   } else if (p.nseg == 1 && (p.seg[0].type == SEG_CSR_FOLD || p.seg[0].type == SEG_CSR_FETCH) &&
@@ -889,11 +821,18 @@ int launch_segments(LaunchParams& p, ElemType t, int op, cudaStream_t stream) {
   return 1;
 }
 
-__global__ void quiesce_kernel(const __grid_constant__ QuiesceParams q, unsigned long long timeout_ns) {
+constexpr int kFlagBatch = 64;
+struct FlagBatch {
+  int n = 0;
+  unsigned long long* flag[kFlagBatch];
+  unsigned long long* seq[kFlagBatch];
+};
+
+__global__ void quiesce_kernel(const __grid_constant__ FlagBatch q, unsigned long long timeout_ns) {
   const int i = threadIdx.x;
   if (i >= q.n) return;
   const unsigned long long t0 = global_ns();
-  const unsigned long long need = *q.count[i];
+  const unsigned long long need = *q.seq[i];
   while (ld_acquire_sys(q.flag[i]) < need) {
     __nanosleep(256);
     if (global_ns() - t0 > timeout_ns) {
@@ -904,9 +843,37 @@ __global__ void quiesce_kernel(const __grid_constant__ QuiesceParams q, unsigned
   }
 }
 
-void launch_quiesce(const QuiesceParams& q, double timeout_s, cudaStream_t s) {
-  if (q.n <= 0) return;
-  quiesce_kernel<<<1, QuiesceParams::kMax, 0, s>>>(q, static_cast<unsigned long long>(timeout_s * 1e9));
+__global__ void signal_kernel(const __grid_constant__ FlagBatch q) {
+  for (int i = 0; i < q.n; ++i) {
+    const unsigned long long v = *q.seq[i] + 1;
+    *q.seq[i] = v;
+    st_release_sys(q.flag[i], v);
+  }
+}
+
+template <class K>
+void batched(unsigned long long* const* flag, unsigned long long* const* seq, int n, K&& k) {
+  for (int b = 0; b < n; b += kFlagBatch) {
+    FlagBatch q;
+    q.n = std::min(kFlagBatch, n - b);
+    for (int i = 0; i < q.n; ++i) {
+      q.flag[i] = flag[b + i];
+      q.seq[i] = seq[b + i];
+    }
+    k(q);
+  }
+}
+
+void launch_signal(unsigned long long* const* flag, unsigned long long* const* seq, int n, cudaStream_t s) {
+  batched(flag, seq, n, [&](const FlagBatch& q) { signal_kernel<<<1, 1, 0, s>>>(q); });
+}
+
+void launch_quiesce(const unsigned long long* const* flag, const unsigned long long* const* count, int n,
+                    double timeout_s, cudaStream_t s) {
+  batched(const_cast<unsigned long long* const*>(flag), const_cast<unsigned long long* const*>(count), n,
+          [&](const FlagBatch& q) {
+            quiesce_kernel<<<1, kFlagBatch, 0, s>>>(q, static_cast<unsigned long long>(timeout_s * 1e9));
+          });
 }
 
 void launch_digest(const void* p, size_t bytes, unsigned long long* out_dev, cudaStream_t s) {

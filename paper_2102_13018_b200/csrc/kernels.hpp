@@ -6,13 +6,11 @@
 //   SEG_PAIR         dst[dpat(i)] (op)= src[spat(i)]  (pack, unpack, local
 //                    scatter; the reference's pack/unpack/scatter loops,
 //                    /root/reference/proj/src/pack.cpp:111-256)
-//   SEG_PAIR_ATOMIC  same with per-element atomics (free-order mode)
 //   SEG_CSR_FOLD     root-sorted fold: root[r] = fold(root[r], contributions
 //                    in the reference's deterministic order) — bit-exact with
 //                    /root/reference/proj/src/ops.cpp:364,367-376
 //   SEG_CSR_FETCH    serialized fetch-and-op over the same CSR
 //                    (/root/reference/proj/src/ops.cpp:521-563)
-//   SEG_ATOMIC_FETCH free-order fetch-and-op with atomics
 // Patterns are Contiguous, Affine3D (start + x + y*s1 + z*s2) or Indexed.
 #pragma once
 
@@ -53,10 +51,8 @@ struct DPat {
 
 enum SegType : int32_t {
   SEG_PAIR = 0,
-  SEG_PAIR_ATOMIC = 1,
   SEG_CSR_FOLD = 2,
   SEG_CSR_FETCH = 3,
-  SEG_ATOMIC_FETCH = 4,
 };
 
 // Buffer slots a segment can address; filled per call.
@@ -138,6 +134,20 @@ struct FlagWait {
 constexpr int kMaxSegs = 12;
 constexpr int kThreads = 256;
 constexpr int kItems = 8;  // work items per thread per block
+constexpr int kMaxShuffle = 16;
+
+// Free-order fetch-and-op serialization (/root/reference/proj/src/ops.cpp:
+// 531-544): the reference shuffles the order in which the contribution
+// groups (self edges, then one group per remote rank) are applied, with
+// Rng(mix_seed(seed ^ opid, rank)). Each root's CSR entries are stored group
+// by group (self entries >= 0 first, then remote stage positions ascending),
+// so the kernel walks the groups' sub-ranges in `perm` order.
+struct FetchShuffle {
+  int32_t n = 0;     // groups (0 or 1: stored order)
+  int32_t self = 0;  // group 0 holds the self edges
+  int32_t perm[kMaxShuffle] = {};
+  int32_t off[kMaxShuffle + 1] = {};  // stage offset where remote group k starts (+ end)
+};
 
 struct LaunchParams {
   DSeg seg[kMaxSegs];
@@ -155,6 +165,7 @@ struct LaunchParams {
   unsigned long long* done_seq[kMaxPeers];
   int ndone = 0;
   unsigned int* done_count = nullptr;
+  FetchShuffle shuf;
 };
 
 // Element type the kernel instantiates for.
@@ -163,16 +174,16 @@ enum class ElemType : int32_t { u8, u16, u32, u64, i32, i64, f64 };
 // Returns number of kernel launches issued (0 or 1 per call).
 int launch_segments(LaunchParams& p, ElemType t, int op, cudaStream_t stream);
 
+// p2p: ++*seq[i] and publish it in flag[i] (system-scope release) for n
+// channels, after everything earlier on the stream (acknowledgements that do
+// not fit one launch's parameter block).
+void launch_signal(unsigned long long* const* flag, unsigned long long* const* seq, int n, cudaStream_t s);
+
 // p2p teardown: wait until every message this slot sent was acknowledged
 // (flag[i] >= *count[i]), so no peer still writes into the slot when it is
-// freed. Gives up with a warning after timeout_s (a dead peer).
-struct QuiesceParams {
-  static constexpr int kMax = 3 * kMaxPeers;
-  int n = 0;
-  const unsigned long long* flag[kMax];
-  const unsigned long long* count[kMax];
-};
-void launch_quiesce(const QuiesceParams& q, double timeout_s, cudaStream_t s);
+// freed. Gives up with a warning after timeout_s (a dead peer). Any n.
+void launch_quiesce(const unsigned long long* const* flag, const unsigned long long* const* count, int n,
+                    double timeout_s, cudaStream_t s);
 
 // Order-independent 64-bit digest of a device buffer (debug checksum).
 void launch_digest(const void* p, size_t bytes, unsigned long long* out_dev, cudaStream_t s);

@@ -22,8 +22,8 @@
 // initial value, self edges by ascending leaf index, then remote ranks
 // ascending, each in ascending leaf index (ops.cpp:364,372-376;
 // oracle.cpp:84-90) — so floating-point results are bit-identical to the CPU
-// reference in both modes (free-order mode keeps an atomics path behind
-// SFG_FREE_ORDER_ATOMICS, pack.cpp:47-58 "atomics" mode).
+// reference. Free-order fetch-and-op applies the contribution groups in the
+// reference's shuffled order (ops.cpp:531-544).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -36,6 +36,28 @@ namespace sfg {
 namespace {
 
 constexpr int kOpReplace = 0;
+
+// The reference's splitmix64 generator and seed mixing
+// (/root/reference/proj/include/sf/rng.hpp:14-51).
+struct SplitMix {
+  uint64_t state;
+  explicit SplitMix(uint64_t seed) : state(seed + 0x9e3779b97f4a7c15ull) {}
+  uint64_t next() {
+    uint64_t z = (state += 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+  }
+  template <class T>
+  void shuffle(std::vector<T>& v) {
+    for (size_t i = v.size(); i > 1; --i) std::swap(v[i - 1], v[next() % i]);
+  }
+};
+
+uint64_t mix_seed(uint64_t seed, uint64_t salt) {
+  SplitMix r(seed ^ (salt * 0xd1342543de82ef95ull + 0x2545f4914f6cdd1dull));
+  return r.next();
+}
 
 DPat contig(int64_t start) {
   DPat p;
@@ -62,8 +84,7 @@ int64_t common_run(const DPat& a, const DPat& b, int64_t n) {
   return g >= 16 && g < (int64_t(1) << 31) ? g : 0;
 }
 
-DSeg pair_seg(const DPat& src, int sbuf, const DPat& dst, int dbuf, int64_t n, bool replace,
-              bool atomic = false) {
+DSeg pair_seg(const DPat& src, int sbuf, const DPat& dst, int dbuf, int64_t n, bool replace) {
   DSeg s;
   s.src = src;
   s.dst = dst;
@@ -71,7 +92,7 @@ DSeg pair_seg(const DPat& src, int sbuf, const DPat& dst, int dbuf, int64_t n, b
   s.dst_buf = dbuf;
   s.n = n;
   s.replace = replace ? 1 : 0;
-  s.type = atomic ? SEG_PAIR_ATOMIC : SEG_PAIR;
+  s.type = SEG_PAIR;
   s.run = common_run(src, dst, n);
   if (s.run) s.rundiv = make_fastdiv(static_cast<uint32_t>(s.run));
   return s;
@@ -147,47 +168,116 @@ DSeg csr_seg(const DevPlan& d, CsrRange range, int32_t type, bool seq, size_t ub
   return s;
 }
 
-// Accumulates the segments of one launch and picks the element type.
+// Accumulates the segments of one operation phase, picks the element type
+// and issues them. A phase is normally ONE kernel launch; when it holds more
+// segments, flag waits or peer buffers than one launch's parameter block
+// (kMaxSegs / kMaxPeers), it is split IN ORDER into several launches on the
+// same stream — puts stay ahead of the receives that wait on peers, and the
+// completion flags (acknowledgements) are raised by the last launch, after
+// every earlier one finished — so any number of neighbour groups works.
 struct Launch {
-  LaunchParams p{};
+  struct Item {
+    DSeg seg;
+    std::vector<int> waits;  // indices into `waits`
+    void* peer = nullptr;    // p2p put: the peer's mapped slot base
+    bool remote_put = false;
+    int64_t entries = 0, distinct_src = 0, distinct_dst = 0;
+  };
+  struct Done {
+    unsigned long long* flag;
+    unsigned long long* seq;
+  };
+  std::vector<Item> items;
+  std::vector<FlagWait> waits;
+  std::vector<Done> dones;
+  unsigned int* done_count = nullptr;
+  void* bufs[BUF_PEER0] = {};
+  FetchShuffle shuffle;
   bool any_op = false;
+  const char* tag = "kernel";
+
+  int nseg() const { return static_cast<int>(items.size()); }
 
   // entries: CSR contributions; src_distinct / dst_distinct: distinct
   // indices of the two patterns (-1 = all distinct), for algorithmic bytes.
-  void add(const DSeg& s, int64_t entries = 0, int64_t src_distinct = -1,
-           int64_t dst_distinct = -1) {
+  void add(const DSeg& s, int64_t entries = 0, int64_t src_distinct = -1, int64_t dst_distinct = -1,
+           std::vector<int> w = {}) {
     if (s.n <= 0) return;
-    SFG_REQUIRE(p.nseg < kMaxSegs, "too many segments in one launch");
-    csr_entries[p.nseg] = entries;
-    distinct_src[p.nseg] = src_distinct < 0 ? s.n : src_distinct;
-    distinct_dst[p.nseg] = dst_distinct < 0 ? s.n : dst_distinct;
-    p.seg[p.nseg++] = s;
+    Item it;
+    it.seg = s;
+    it.seg.wait_mask = 0;
+    it.waits = std::move(w);
+    it.entries = entries;
+    it.distinct_src = src_distinct < 0 ? s.n : src_distinct;
+    it.distinct_dst = dst_distinct < 0 ? s.n : dst_distinct;
     if (!s.replace) any_op = true;
+    items.push_back(std::move(it));
+  }
+
+  // Append another phase's segments (its own buffers are the same slots).
+  void absorb(const Launch& o) {
+    for (const auto& it : o.items) {
+      Item c = it;
+      for (int& w : c.waits) w += static_cast<int>(waits.size());
+      items.push_back(std::move(c));
+      if (!it.seg.replace) any_op = true;
+    }
+    waits.insert(waits.end(), o.waits.begin(), o.waits.end());
+  }
+
+  // p2p: wait until *flag >= *count + delta; returns the wait's index.
+  int add_wait(const unsigned long long* flag, const unsigned long long* count, uint64_t delta) {
+    waits.push_back(FlagWait{flag, count, delta});
+    return static_cast<int>(waits.size()) - 1;
+  }
+
+  // p2p: once every CTA of the phase is done, ++*seq and publish it in flag.
+  void add_done(unsigned long long* flag, unsigned long long* seq, unsigned int* counter) {
+    dones.push_back(Done{flag, seq});
+    done_count = counter;
+  }
+
+  // One-sided put into a peer's slot (p2p) at vertex offset `peer_off`; it
+  // waits for `wait`, and its completion advances *seq and publishes it in
+  // `flag` (sig_count: the segment's CTA arrival counter).
+  void add_put(const DPat& src, int sbuf, void* base, int64_t peer_off, int64_t n, int wait,
+               unsigned int* sig_count, unsigned long long* flag, unsigned long long* seq, bool remote,
+               int64_t src_distinct = -1) {
+    DSeg s = pair_seg(src, sbuf, contig(peer_off), BUF_PEER0, n, true);
+    s.sig_count = sig_count;
+    s.sig_flag = flag;
+    s.sig_seq = seq;
+    add(s, 0, src_distinct, -1, {wait});
+    items.back().peer = base;
+    items.back().remote_put = remote;
   }
 
   void run(const Unit& u, ReduceOp op, cudaStream_t st) {
-    if (p.nseg == 0) return;
+    if (items.empty()) return;
     ElemType t;
     int kop = static_cast<int>(op);
+    int64_t bl = 1;
     if (!any_op) {
       // Verbatim move: widest word that divides the vertex size and the
       // alignment of every buffer involved.
       uintptr_t align = u.bytes();
-      for (int b = 0; b < BUF_COUNT; ++b)
-        if (p.bufs[b]) align |= reinterpret_cast<uintptr_t>(p.bufs[b]);
+      for (int b = 0; b < BUF_PEER0; ++b)
+        if (bufs[b]) align |= reinterpret_cast<uintptr_t>(bufs[b]);
+      for (const auto& it : items)
+        if (it.peer) align |= reinterpret_cast<uintptr_t>(it.peer);
       const size_t ub = u.bytes();
       if ((align & 7) == 0) {
         t = ElemType::u64;
-        p.bl = static_cast<int64_t>(ub / 8);
+        bl = static_cast<int64_t>(ub / 8);
       } else if ((align & 3) == 0) {
         t = ElemType::u32;
-        p.bl = static_cast<int64_t>(ub / 4);
+        bl = static_cast<int64_t>(ub / 4);
       } else if ((align & 1) == 0) {
         t = ElemType::u16;
-        p.bl = static_cast<int64_t>(ub / 2);
+        bl = static_cast<int64_t>(ub / 2);
       } else {
         t = ElemType::u8;
-        p.bl = static_cast<int64_t>(ub);
+        bl = static_cast<int64_t>(ub);
       }
       kop = kOpReplace;
     } else {
@@ -197,7 +287,7 @@ struct Launch {
         case Kind::float64: t = ElemType::f64; break;
         default: fail("reduction requires a non-opaque unit kind");
       }
-      p.bl = u.blocklen;
+      bl = u.blocklen;
     }
     const bool timed = timing_enabled();
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -206,37 +296,91 @@ struct Launch {
       e1 = timing_event();
       SFG_CUDA(cudaEventRecord(e0, st));
     }
-    const int launched = launch_segments(p, t, kop, st);
-    SFG_REQUIRE(launched >= 0, "no kernel instantiation for this unit/op combination");
-    SFG_CUDA(cudaGetLastError());
+    // Greedy in-order split into launches that fit the parameter block.
+    size_t i = 0;
+    int launched = 0;
+    while (i < items.size()) {
+      LaunchParams p{};
+      std::copy(bufs, bufs + BUF_PEER0, p.bufs);
+      p.bl = bl;
+      p.shuf = shuffle;
+      std::vector<int> wmap(waits.size(), -1);
+      int nw = 0, npeer = 0;
+      while (i < items.size() && p.nseg < kMaxSegs) {
+        const Item& it = items[i];
+        int need = 0;
+        for (int w : it.waits)
+          if (wmap[static_cast<size_t>(w)] < 0) ++need;
+        if (p.nseg > 0 && (nw + need > kMaxPeers || (it.peer && npeer + 1 > kMaxPeers))) break;
+        SFG_REQUIRE(need <= kMaxPeers, "one segment waits on more than kMaxPeers flags");
+        DSeg s = it.seg;
+        for (int w : it.waits) {
+          int& m = wmap[static_cast<size_t>(w)];
+          if (m < 0) {
+            m = nw++;
+            p.waits[m] = waits[static_cast<size_t>(w)];
+          }
+          s.wait_mask |= 1u << m;
+        }
+        if (it.peer) {
+          s.dst_buf = BUF_PEER0 + npeer;
+          p.bufs[BUF_PEER0 + npeer] = it.peer;
+          ++npeer;
+        }
+        p.seg[p.nseg++] = s;
+        ++i;
+      }
+      const bool last = i == items.size();
+      if (last && static_cast<int>(dones.size()) <= kMaxPeers) {
+        for (const auto& d : dones) {
+          p.done_flag[p.ndone] = d.flag;
+          p.done_seq[p.ndone] = d.seq;
+          ++p.ndone;
+        }
+        p.done_count = done_count;
+      }
+      const int r = launch_segments(p, t, kop, st);
+      SFG_REQUIRE(r >= 0, "no kernel instantiation for this unit/op combination");
+      SFG_CUDA(cudaGetLastError());
+      launched += r;
+      if (last && static_cast<int>(dones.size()) > kMaxPeers) {
+        // more acknowledgements than one parameter block holds: raise them
+        // from a signalling kernel behind the data launches
+        std::vector<unsigned long long*> f, q;
+        for (const auto& d : dones) {
+          f.push_back(d.flag);
+          q.push_back(d.seq);
+        }
+        launch_signal(f.data(), q.data(), static_cast<int>(f.size()), st);
+        ++launched;
+      }
+    }
     counters().kernel_launches += static_cast<uint64_t>(launched);
     if (timed) {
       SFG_CUDA(cudaEventRecord(e1, st));
       double link = 0;
-      for (int s = 0; s < p.nseg; ++s) link += remote_put[s] ? static_cast<double>(p.seg[s].n) * u.bytes() : 0.0;
+      for (const auto& it : items) link += it.remote_put ? static_cast<double>(it.seg.n) * u.bytes() : 0.0;
       timing_record(tag, e0, e1, algorithmic_bytes(u), link);
     }
   }
 
-  // Compulsory bytes of this launch: every element read once and written
+  // Compulsory bytes of this phase: every element read once and written
   // once, destination reads for reductions, int32 indices of Indexed
   // patterns; affine/contiguous patterns cost no index traffic.
   double algorithmic_bytes(const Unit& u) const {
     const double ub = static_cast<double>(u.bytes());
     double b = 0;
-    for (int s = 0; s < p.nseg; ++s) {
-      const DSeg& g = p.seg[s];
+    for (const auto& it : items) {
+      const DSeg& g = it.seg;
       const double n = static_cast<double>(g.n);
       const double idx = 4.0 * n * ((g.src.kind == PAT_INDEXED) + (g.dst.kind == PAT_INDEXED));
-      const double ds = static_cast<double>(distinct_src[s]);
-      const double dd = static_cast<double>(distinct_dst[s]);
+      const double ds = static_cast<double>(it.distinct_src);
+      const double dd = static_cast<double>(it.distinct_dst);
       switch (g.type) {
-        case SEG_PAIR:
-        case SEG_PAIR_ATOMIC: b += ds * ub + dd * ub * (g.replace ? 1.0 : 2.0) + idx; break;
-        case SEG_ATOMIC_FETCH: b += 2.0 * n * ub + 2.0 * dd * ub + idx; break;
+        case SEG_PAIR: b += ds * ub + dd * ub * (g.replace ? 1.0 : 2.0) + idx; break;
         case SEG_CSR_FOLD:
         case SEG_CSR_FETCH: {
-          const double e = static_cast<double>(csr_entries[s]);
+          const double e = static_cast<double>(it.entries);
           b += n * ub * 2.0 + e * ub * (g.type == SEG_CSR_FETCH ? 2.0 : 1.0) + 4.0 * e + 12.0 * n;
           break;
         }
@@ -244,61 +388,18 @@ struct Launch {
     }
     return b;
   }
-
-  // p2p: wait until *flag >= *count + delta; returns the segment mask bit.
-  uint32_t add_wait(const unsigned long long* flag, const unsigned long long* count, uint64_t delta) {
-    SFG_REQUIRE(nwait < kMaxPeers, "p2p: too many flag waits in one launch");
-    p.waits[nwait].flag = flag;
-    p.waits[nwait].count = count;
-    p.waits[nwait].delta = delta;
-    return 1u << nwait++;
-  }
-
-  // p2p: once every CTA of the launch is done, ++*seq and publish it in flag.
-  void add_done(unsigned long long* flag, unsigned long long* seq, unsigned int* counter) {
-    SFG_REQUIRE(p.ndone < kMaxPeers, "p2p: too many completion flags in one launch");
-    p.done_flag[p.ndone] = flag;
-    p.done_seq[p.ndone] = seq;
-    p.done_count = counter;
-    ++p.ndone;
-  }
-
-  // One-sided put into a peer's slot (p2p): the segment's destination is
-  // buffer `BUF_PEER0 + k` = `base`; it waits for `wait_mask`, and its
-  // completion advances *seq and publishes it in `flag`.
-  void add_put(const DPat& src, int sbuf, int k, void* base, int64_t peer_off, int64_t n,
-               uint32_t wait_mask, unsigned int* counters, unsigned long long* flag,
-               unsigned long long* seq, bool remote, int64_t src_distinct = -1) {
-    SFG_REQUIRE(k < kMaxPeers, "p2p: too many neighbor groups in one launch");
-    DSeg s = pair_seg(src, sbuf, contig(peer_off), BUF_PEER0 + k, n, true);
-    s.wait_mask = wait_mask;
-    s.sig_count = counters + k;
-    s.sig_flag = flag;
-    s.sig_seq = seq;
-    p.bufs[BUF_PEER0 + k] = base;
-    remote_put[p.nseg] = remote;
-    add(s, 0, src_distinct);
-  }
-
-  int nwait = 0;
-
-  const char* tag = "kernel";
-  bool remote_put[kMaxSegs] = {};
-  int64_t csr_entries[kMaxSegs] = {};
-  int64_t distinct_src[kMaxSegs] = {};
-  int64_t distinct_dst[kMaxSegs] = {};
 };
 
 void set_bufs(Launch& L, const OpHandle& h, void* root, void* leaf, const void* src_ro) {
-  L.p.bufs[BUF_ROOT] = root;
-  L.p.bufs[BUF_LEAF] = leaf;
-  L.p.bufs[BUF_SRC_RO] = const_cast<void*>(src_ro);
+  L.bufs[BUF_ROOT] = root;
+  L.bufs[BUF_LEAF] = leaf;
+  L.bufs[BUF_SRC_RO] = const_cast<void*>(src_ro);
   if (h.stg) {
-    L.p.bufs[BUF_LEAF_STAGE] = h.stg->leaf_stage;
-    L.p.bufs[BUF_ROOT_STAGE] = h.stg->root_stage;
-    L.p.bufs[BUF_LEAF_REPLY] = h.stg->leaf_reply;
+    L.bufs[BUF_LEAF_STAGE] = h.stg->leaf_stage;
+    L.bufs[BUF_ROOT_STAGE] = h.stg->root_stage;
+    L.bufs[BUF_LEAF_REPLY] = h.stg->leaf_reply;
   }
-  L.p.bufs[BUF_LEAFUPDATE] = h.leafupdate;
+  L.bufs[BUF_LEAFUPDATE] = h.leafupdate;
 }
 
 uint64_t data_tag(uint64_t opid) { return opid * 2; }
@@ -323,6 +424,9 @@ void begin_common(OpHandle& h, const void* ck_ptr, size_t ck_bytes) {
   StarForest& sf = *h.sf;
   sf.comm().bind_device();
   h.opid = sf.comm().next_op_seq();
+  SFG_REQUIRE(sf.prepared() || !stream_capturing(h.stream),
+              "first operation on a forest inside a CUDA graph capture: call prepare(unit) on the "
+              "set-up forest before capturing");
   (void)sf.dev();
   h.stg = sf.acquire_staging(h.unit.bytes(), h.stream);
   if (sf.comm().config().debug_checksum && ck_ptr != nullptr && ck_bytes > 0) {
@@ -348,17 +452,9 @@ void end_common(OpHandle& h) {
 // Root-sorted CSR execution for every reduction with duplicate roots, in
 // both modes: the thread-per-root fold beats native atomics at every degree
 // measured (config 1, degree 4: 44.5 us vs 54.8 us; config 4, degree 256:
-// 164 us vs contended atomics) and is bit-exact. Free-order mode keeps the
-// atomics path behind SFG_FREE_ORDER_ATOMICS for ablation.
-bool prefer_csr(StarForest& sf, bool det, CsrRange range) {
-  (void)range;
-  if (!det) {
-    static const bool atomics_only = std::getenv("SFG_FREE_ORDER_ATOMICS") != nullptr;
-    if (atomics_only) return false;
-  }
-  sf.ensure_csr();
-  return true;
-}
+// 164 us vs contended atomics, profiles/r1_configs.md) and is bit-exact, so
+// the free-order atomics variant was removed in round 2.
+void use_csr(StarForest& sf) { sf.ensure_csr(); }
 
 // Reduce with self edges and remote contributions: Begin's local reduction
 // skips the "coupled" roots (those that also receive remote contributions)
@@ -412,8 +508,7 @@ void begin_phase(OpHandle& h, Launch& pack, Launch& local, const std::vector<Xfe
   c.fork(h.stream);
   const bool fuse = local.algorithmic_bytes(h.unit) < kFuseLocalBytes;
   if (fuse) {
-    for (int i = 0; i < local.p.nseg; ++i)
-      pack.add(local.p.seg[i], local.csr_entries[i], local.distinct_src[i], local.distinct_dst[i]);
+    pack.absorb(local);
     pack.tag = tag_of(h, 0);
   } else {
     pack.tag = tag_of(h, 2);
@@ -469,7 +564,7 @@ bool use_p2p(const OpHandle& h) { return h.sf->comm().p2p() && h.stg && h.stg->f
 void p2p_begin(OpHandle& h, Launch& pack, Launch& local,
                const std::function<void(Launch&)>& append_last = nullptr) {
   Comm& c = h.sf->comm();
-  h.xfer = pack.p.nseg > 0;
+  h.xfer = pack.nseg() > 0;
   h.forked = false;
   if (!h.xfer) {
     local.tag = tag_of(h, 0);
@@ -480,8 +575,7 @@ void p2p_begin(OpHandle& h, Launch& pack, Launch& local,
   c.fork(h.stream);
   h.forked = true;
   if (local.algorithmic_bytes(h.unit) < kFuseLocalBytes) {
-    for (int i = 0; i < local.p.nseg; ++i)
-      pack.add(local.p.seg[i], local.csr_entries[i], local.distinct_src[i], local.distinct_dst[i]);
+    pack.absorb(local);
     pack.tag = tag_of(h, 0);
     if (append_last) append_last(pack);
     pack.run(h.unit, h.op, cs);
@@ -518,23 +612,23 @@ void add_puts(OpHandle& h, Launch& L, const std::vector<DevPlan::Seg>& groups, b
     const int64_t off = region == 1 ? ps.root_off : ps.leaf_off;
     SFG_REQUIRE(off >= 0, "p2p: peer slot has no group for this rank");
     // my previous messages into this region of g.rank consumed
-    const uint32_t wm = L.add_wait(s.free_flag(region, g.rank), s.sent(region, g.rank), 0);
-    L.add_put(use_pat ? g.pat : contig(g.stage_off), sbuf, static_cast<int>(k), base, off, g.n, wm,
-              s.seg_counts, s.peer_arrive_flag(region, g.rank, me), s.sent(region, g.rank),
-              g.rank != me, use_pat ? g.distinct : -1);
+    const int w = L.add_wait(s.free_flag(region, g.rank), s.sent(region, g.rank), 0);
+    L.add_put(use_pat ? g.pat : contig(g.stage_off), sbuf, base, off, g.n, w, s.seg_count(region, g.rank),
+              s.peer_arrive_flag(region, g.rank, me), s.sent(region, g.rank), g.rank != me,
+              use_pat ? g.distinct : -1);
     if (g.rank != me) counters().bytes_sent += static_cast<uint64_t>(g.n) * ub;
     counters().pack_copies++;
   }
 }
 
-// The next message from each group's rank: returns the wait bit per group
+// The next message from each group's rank: returns the wait index per group
 // (in group order) and, when `ack` is set, makes the launch acknowledge the
 // messages (sender's free flag) once it is done.
-std::vector<uint32_t> add_receives(OpHandle& h, Launch& L, const std::vector<DevPlan::Seg>& groups,
-                                   int region, bool ack) {
+std::vector<int> add_receives(OpHandle& h, Launch& L, const std::vector<DevPlan::Seg>& groups,
+                              int region, bool ack) {
   Staging& s = *h.stg;
   const int me = h.sf->comm().rank();
-  std::vector<uint32_t> bits;
+  std::vector<int> bits;
   for (const auto& g : groups) {
     // the next message from g.rank arrived: arrive >= recvd + 1
     bits.push_back(L.add_wait(s.arrive_flag(region, g.rank), s.recvd(region, g.rank), 1));
@@ -572,17 +666,19 @@ void begin_root_to_leaf(OpHandle& h) {
     // exchange. Leafdata belongs to the operation between Begin and End.
     static const bool no_fuse = std::getenv("SFG_P2P_NO_FUSED_UNPACK") != nullptr;
     h.fused_unpack = false;
+    // Not when a group is my own rank (force_remote): its unpack CTAs would
+    // wait on put CTAs of the same grid.
+    const int me = sf.comm().rank();
+    const bool self_group =
+        std::any_of(d.rg.begin(), d.rg.end(), [me](const DevPlan::Seg& g) { return g.rank == me; });
     auto fuse = [&](Launch& L) {
       const size_t ng = d.rg.size();
-      if (no_fuse || ng == 0 || L.p.nseg + ng > static_cast<size_t>(kMaxSegs) ||
-          L.nwait + ng > static_cast<size_t>(kMaxPeers) || L.p.ndone + ng > static_cast<size_t>(kMaxPeers))
-        return;
+      if (no_fuse || ng == 0 || self_group) return;
       const auto bits = add_receives(h, L, d.rg, 0, true);
       for (size_t k = 0; k < ng; ++k) {
         const auto& g = d.rg[k];
         DSeg sg = pair_seg(contig(g.stage_off), BUF_LEAF_STAGE, g.pat, BUF_LEAF, g.n, replace);
-        sg.wait_mask = bits[k];
-        L.add(sg);
+        L.add(sg, 0, -1, -1, {bits[k]});
         counters().unpack_copies++;
       }
       h.fused_unpack = true;
@@ -639,8 +735,7 @@ void end_root_to_leaf(OpHandle& h) {
     for (size_t k = 0; k < d.rg.size(); ++k) {
       const auto& g = d.rg[k];
       DSeg s = pair_seg(contig(g.stage_off), BUF_LEAF_STAGE, g.pat, BUF_LEAF, g.n, replace);
-      s.wait_mask = bits[k];
-      L.add(s);
+      L.add(s, 0, -1, -1, {bits[k]});
       counters().unpack_copies++;
     }
     L.run(h.unit, h.op, h.forked ? c.comm_stream() : h.stream);
@@ -694,16 +789,14 @@ void begin_leaf_to_root(OpHandle& h) {
     if (replace || !d.self_root_dups) {
       local.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, replace), 0, -1,
                 d.self_root_distinct);
-    } else if (prefer_csr(sf, det, CsrRange::self_only)) {
-      local.add(csr_seg(d, CsrRange::self_only, SEG_CSR_FOLD, exact_seq(h, det), h.unit.bytes()), d.csr_self_entries);
     } else {
-      local.add(pair_seg(d.self_leaf, BUF_LEAF, d.self_root, BUF_ROOT, d.n_self, false, true), 0, -1,
-                d.self_root_distinct);
+      use_csr(sf);
+      local.add(csr_seg(d, CsrRange::self_only, SEG_CSR_FOLD, exact_seq(h, det), h.unit.bytes()), d.csr_self_entries);
     }
   }
   h.coupled_split = split_coupled(sf, h);
   if (h.coupled_split)
-    for (int i = 0; i < local.p.nseg; ++i) local.p.seg[i].skip_dst = d.coupled_bits;
+    for (auto& it : local.items) it.seg.skip_dst = d.coupled_bits;
   if (p2p) {
     p2p_begin(h, pack, local);
     return;
@@ -729,7 +822,8 @@ void end_leaf_to_root(OpHandle& h) {
   Launch L;
   L.tag = tag_of(h, 1);
   set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
-  std::vector<uint32_t> bits(d.lg.size(), 0);
+  std::vector<int> bits;
+  auto wait_k = [&bits](size_t k) { return bits.empty() ? std::vector<int>{} : std::vector<int>{bits[k]}; };
   Comm& c = sf.comm();
   if (h.coupled_split) {
     // Whole fold of the coupled roots, concurrent with Begin's local part.
@@ -739,8 +833,7 @@ void end_leaf_to_root(OpHandle& h) {
     s.csr_lo = d.ccsr_lo;
     s.csr_hi = d.ccsr_hi;
     s.csr_ent = d.csr_ent;
-    for (uint32_t b : bits) s.wait_mask |= b;
-    L.add(s, d.ccsr_entries);
+    L.add(s, d.ccsr_entries, -1, -1, bits);
     counters().unpack_copies += d.lg.size();
     if (p2p) {
       L.run(h.unit, h.op, h.forked ? c.comm_stream() : h.stream);
@@ -767,24 +860,15 @@ void end_leaf_to_root(OpHandle& h) {
         if (!h.zero_copy_recv.empty() && h.zero_copy_recv[k]) continue;
         const auto& g = d.lg[k];
         DSeg s = pair_seg(contig(g.stage_off), BUF_ROOT_STAGE, g.pat, BUF_ROOT, g.n, replace);
-        s.wait_mask = bits[k];
-        L.add(s, 0, -1, g.distinct);
+        L.add(s, 0, -1, g.distinct, wait_k(k));
         counters().unpack_copies++;
       }
-    } else if (prefer_csr(sf, det, CsrRange::remote_only)) {
-      // Ascending-rank fold of every remote contribution (ops.cpp:372-376).
-      DSeg s = csr_seg(d, CsrRange::remote_only, SEG_CSR_FOLD, exact_seq(h, det), h.unit.bytes());
-      for (uint32_t b : bits) s.wait_mask |= b;
-      L.add(s, d.csr_remote_entries);
-      counters().unpack_copies += d.lg.size();
     } else {
-      for (size_t k = 0; k < d.lg.size(); ++k) {
-        const auto& g = d.lg[k];
-        DSeg s = pair_seg(contig(g.stage_off), BUF_ROOT_STAGE, g.pat, BUF_ROOT, g.n, false, true);
-        s.wait_mask = bits[k];
-        L.add(s, 0, -1, g.distinct);
-        counters().unpack_copies++;
-      }
+      // Ascending-rank fold of every remote contribution (ops.cpp:372-376).
+      use_csr(sf);
+      DSeg s = csr_seg(d, CsrRange::remote_only, SEG_CSR_FOLD, exact_seq(h, det), h.unit.bytes());
+      L.add(s, d.csr_remote_entries, -1, -1, bits);
+      counters().unpack_copies += d.lg.size();
     }
   }
   L.run(h.unit, h.op, h.stream);
@@ -829,7 +913,7 @@ void end_fetch(OpHandle& h) {
   Launch L;
   L.tag = "fetch_end";
   set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
-  std::vector<uint32_t> bits(d.lg.size(), 0);
+  std::vector<int> bits;
   if (p2p) {
     p2p_join(h);
     // Consumed (acknowledged) only after the replies have been read out of
@@ -838,29 +922,27 @@ void end_fetch(OpHandle& h) {
   } else {
     end_wait(h, data_tag(h.opid), h.recvs);
   }
-  if (!d.rg.empty() && h.stg->leaf_reply == nullptr && h.stg->leaf_bytes)
-    SFG_CUDA(cudaMalloc(&h.stg->leaf_reply, h.stg->leaf_bytes));
 
-  // Root side: serialize every contribution per root.
-  if (prefer_csr(sf, det, CsrRange::all)) {
-    DSeg s = csr_seg(d, CsrRange::all, SEG_CSR_FETCH, exact_seq(h, det), h.unit.bytes());
-    for (uint32_t b : bits) s.wait_mask |= b;
-    L.add(s, d.csr_self_entries + d.csr_remote_entries);
-  } else {
-    if (d.has_self) {
-      DSeg s = pair_seg(d.self_leaf, BUF_SRC_RO, d.self_root, BUF_ROOT, d.n_self, false);
-      s.type = SEG_ATOMIC_FETCH;
-      s.aux_buf = BUF_LEAFUPDATE;
-      L.add(s);
-    }
-    for (size_t k = 0; k < d.lg.size(); ++k) {
-      const auto& g = d.lg[k];
-      DSeg s = pair_seg(contig(g.stage_off), BUF_ROOT_STAGE, g.pat, BUF_ROOT, g.n, false);
-      s.type = SEG_ATOMIC_FETCH;
-      s.aux_buf = BUF_ROOT_STAGE;
-      s.wait_mask = bits[k];
-      L.add(s);
-    }
+  // Root side: serialize every contribution per root. Deterministic mode:
+  // the reference order (self, then ascending rank). Free-order mode: the
+  // groups in the reference's shuffled order (ops.cpp:531-544), a genuinely
+  // different serialization per operation.
+  use_csr(sf);
+  DSeg s = csr_seg(d, CsrRange::all, SEG_CSR_FETCH, exact_seq(h, det), h.unit.bytes());
+  L.add(s, d.csr_self_entries + d.csr_remote_entries, -1, -1, bits);
+  const int ngroups = (d.has_self ? 1 : 0) + static_cast<int>(d.lg.size());
+  if (!det && ngroups > 1 && ngroups <= kMaxShuffle) {
+    FetchShuffle& f = L.shuffle;
+    f.n = ngroups;
+    f.self = d.has_self ? 1 : 0;
+    for (size_t k = 0; k < d.lg.size(); ++k) f.off[k] = static_cast<int32_t>(d.lg[k].stage_off);
+    f.off[d.lg.size()] = static_cast<int32_t>(d.n_rootside);
+    std::vector<int32_t> order(static_cast<size_t>(ngroups));
+    for (int g = 0; g < ngroups; ++g) order[static_cast<size_t>(g)] = g;
+    SplitMix rng(mix_seed(c.config().seed ^ h.opid, static_cast<uint64_t>(c.rank())));
+    rng.shuffle(order);
+    for (int g = 0; g < ngroups; ++g) f.perm[g] = order[static_cast<size_t>(g)];
+    h.fetch_order.assign(order.begin(), order.end());
   }
   L.run(h.unit, h.op, h.stream);
 
@@ -879,8 +961,7 @@ void end_fetch(OpHandle& h) {
     for (size_t k = 0; k < d.rg.size(); ++k) {
       const auto& g = d.rg[k];
       DSeg s = pair_seg(contig(g.stage_off), BUF_LEAF_REPLY, g.pat, BUF_LEAFUPDATE, g.n, true);
-      s.wait_mask = rbits[k];
-      U.add(s);
+      U.add(s, 0, -1, -1, {rbits[k]});
       counters().unpack_copies++;
     }
     U.run(h.unit, ReduceOp::replace, h.stream);

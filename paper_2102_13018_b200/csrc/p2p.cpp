@@ -44,14 +44,12 @@ void StarForest::p2p_attach(Staging& s) {
   Comm& c = *comm_;
   const int P = c.size();
   const int me = c.rank();
-  SFG_REQUIRE(static_cast<int>(d.rg.size()) <= kMaxPeers && static_cast<int>(d.lg.size()) <= kMaxPeers,
-              "p2p backend supports at most 16 neighbor ranks per forest");
   s.nranks = P;
   const size_t root_at = align256(s.leaf_bytes);
   const size_t reply_at = root_at + align256(s.root_bytes);
   const size_t flags_at = reply_at + align256(s.leaf_bytes);
   const size_t flag_bytes = 12 * static_cast<size_t>(P) * sizeof(unsigned long long) +
-                            (kMaxPeers + 1) * sizeof(unsigned int);
+                            (3 * static_cast<size_t>(P) + 1) * sizeof(unsigned int);
   const size_t total = flags_at + align256(flag_bytes);
   SFG_CUDA(cudaMalloc(&s.slot_mem, total));
   char* base = static_cast<char*>(s.slot_mem);
@@ -60,7 +58,7 @@ void StarForest::p2p_attach(Staging& s) {
   s.leaf_reply = s.leaf_bytes ? base + reply_at : nullptr;
   s.flags = reinterpret_cast<unsigned long long*>(base + flags_at);
   s.seg_counts = reinterpret_cast<unsigned int*>(s.flags + 12 * P);
-  s.done_count = s.seg_counts + kMaxPeers;
+  s.done_count = s.seg_counts + 3 * P;
   SFG_CUDA(cudaMemset(s.flags, 0, flag_bytes));
   SFG_CUDA(cudaDeviceSynchronize());  // flags are zero before any peer can see them
 

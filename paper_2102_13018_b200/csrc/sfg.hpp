@@ -274,7 +274,11 @@ class Comm {
   CommConfig& config_mut() { return cfg_; }
   ControlPlane& ctrl() { return *ctrl_; }
   Transport& transport();
-  uint64_t next_op_seq() { return ++op_seq_; }
+  // Operation ids 0, 1, 2, ... per communicator, as the reference's
+  // Comm::next_op_seq (comm.cpp:184-186: fetch_add from 0); they seed the
+  // free-order fetch shuffle, so the same sequence of calls serializes
+  // exactly as the reference does.
+  uint64_t next_op_seq() { return op_seq_++; }
   void bind_device() const;
   // One-sided put/signal data plane over NVLink peer mappings (backend "p2p").
   bool p2p() const { return cfg_.backend == "p2p"; }
@@ -413,12 +417,14 @@ struct Staging {
   bool released_recorded = false;
   unsigned long long released_capture = 0;  // capture id the release was recorded in (0: none)
   bool in_use = false;
+  bool retired = false;  // freed handle never ended (p2p): never reused
   size_t leaf_bytes = 0, root_bytes = 0;
   // p2p: one allocation holding the three stages (regions: 0 leaf stage,
   // 1 root stage, 2 leaf reply) and the flags
   //   arrive[3][P], free[3][P]  (uint64, written by peers)
   //   sent[3][P], recvd[3][P]   (uint64 local message counters)
-  //   seg_counts[kMaxPeers], done_count (uint32 CTA arrival counters)
+  //   seg_counts[3][P], done_count (uint32 CTA arrival counters: one per
+  //   put channel, one for the launches that acknowledge)
   // Per directed pair and region: the n-th put from me into region g of
   // peer d waits for free[g][d] >= n-1 (d consumed my previous message
   // there) and raises d.arrive[g][me] = n; the n-th message from s into my
@@ -434,6 +440,7 @@ struct Staging {
   int nranks = 0;
   unsigned long long* sent(int g, int r) const { return flags + (6 + g) * nranks + r; }
   unsigned long long* recvd(int g, int r) const { return flags + (9 + g) * nranks + r; }
+  unsigned int* seg_count(int g, int r) const { return seg_counts + g * nranks + r; }
   std::vector<PeerSlot> peers;  // by rank
   const unsigned long long* arrive_flag(int g, int src) const { return flags + g * nranks + src; }
   const unsigned long long* free_flag(int g, int dst) const { return flags + (3 + g) * nranks + dst; }
@@ -484,6 +491,15 @@ class StarForest {
   DevPlan& dev();
   void ensure_csr();
   void ensure_csr_host();
+  // Everything the first operation of unit size `ub` would otherwise build
+  // inside Begin/End (host syncs, cudaMalloc, the p2p slot's collective
+  // attachment): the device plan, the root-sorted CSR when some root has
+  // several leaves, and a free staging slot of that unit size. Collective
+  // (p2p). SetUp calls it for 8-byte units on a device communicator; after
+  // it, such operations can be captured into a CUDA graph from the start.
+  void prepare(size_t ub);
+  void prepare_default();
+  bool prepared() const;  // device plan (+ CSR where needed) built
   Staging* acquire_staging(size_t ub, cudaStream_t stream);
   void release_staging(Staging* s, cudaStream_t stream);
   void p2p_attach(Staging& s);  // collective: allocate the slot, map it into the neighbors
@@ -510,6 +526,8 @@ class StarForest {
   std::vector<std::unique_ptr<Staging>> staging_;
 };
 
+bool stream_capturing(cudaStream_t s);
+
 // ------------------------------------------------------------ operations
 // /root/reference/proj/include/sf/ops.hpp:14-94
 enum class OpKind : uint8_t { bcast = 0, reduce, fetch_and_op, gather, scatter };
@@ -533,6 +551,7 @@ struct OpHandle {
   bool fused_unpack = false;        // p2p Bcast: the unpack ran in the put launch
   bool coupled_split = false;       // reduce: coupled roots folded in End (DevPlan::coupled_bits)
   std::vector<uint8_t> zero_copy_recv;
+  std::vector<int32_t> fetch_order;  // free-order fetch: group order used (empty: stored order)
   // debug checksum
   const void* ck_ptr = nullptr;
   size_t ck_bytes = 0;

@@ -59,15 +59,14 @@ Staging::~Staging() {
   if (slot_mem && flags && !no_quiesce) {
     // Peers acknowledge my puts by writing into this slot after their
     // unpacks; wait for the last acknowledgement before freeing it.
-    QuiesceParams q;
+    std::vector<const unsigned long long*> f, c;
     for (int g = 0; g < 3; ++g)
       for (int r = 0; r < nranks && r < static_cast<int>(peers.size()); ++r)
-        if (peers[static_cast<size_t>(r)].base && q.n < QuiesceParams::kMax) {
-          q.flag[q.n] = free_flag(g, r);
-          q.count[q.n] = sent(g, r);
-          ++q.n;
+        if (peers[static_cast<size_t>(r)].base) {
+          f.push_back(free_flag(g, r));
+          c.push_back(sent(g, r));
         }
-    launch_quiesce(q, 10.0, cudaStreamPerThread);
+    launch_quiesce(f.data(), c.data(), static_cast<int>(f.size()), 10.0, cudaStreamPerThread);
     cudaStreamSynchronize(cudaStreamPerThread);
   }
   for (auto& p : peers)
@@ -306,6 +305,17 @@ void StarForest::setup(SetupAlg alg) {
   root_groups_ = std::move(roots);
   leaf_groups_ = std::move(leaves);
   state_ = SfState::set_up;
+  prepare_default();
+  pt.mark("device plan + staging");
+}
+
+// SetUp's last step on a device communicator: the device plan, the CSR and
+// one 8-byte staging slot, so that no Begin/End of an 8-byte unit allocates
+// or synchronises (and a first operation can be graph-captured).
+void StarForest::prepare_default() {
+  if (!comm_->has_device()) return;
+  comm_->bind_device();
+  prepare(8);
 }
 
 const std::vector<Group>& StarForest::root_groups() const {
@@ -692,10 +702,27 @@ void StarForest::ensure_csr_host() {
   d.csr_built = true;
 }
 
+bool StarForest::prepared() const {
+  return dev_ && dev_->built && (dev_->csr_built || !(dev_->self_root_dups || dev_->remote_root_dups));
+}
+
+bool stream_capturing(cudaStream_t s) { return capture_id(s) != 0; }
+
+void StarForest::prepare(size_t ub) {
+  require_state(SfState::set_up, "prepare");
+  if (!comm_->has_device()) return;
+  DevPlan& d = dev();
+  if ((d.self_root_dups || d.remote_root_dups) && !d.csr_built) ensure_csr();
+  for (auto& s : staging_)
+    if (!s->in_use && !s->retired && s->unit_bytes == ub) return;
+  release_staging(acquire_staging(ub, cudaStreamPerThread), cudaStreamPerThread);
+  SFG_CUDA(cudaStreamSynchronize(cudaStreamPerThread));
+}
+
 Staging* StarForest::acquire_staging(size_t ub, cudaStream_t stream) {
   DevPlan& d = dev();
   for (auto& s : staging_) {
-    if (s->in_use || s->unit_bytes != ub) continue;
+    if (s->in_use || s->retired || s->unit_bytes != ub) continue;
     s->in_use = true;
     if (s->released_recorded && s->released_capture == capture_id(stream))
       SFG_CUDA(cudaStreamWaitEvent(stream, s->released, 0));
@@ -703,6 +730,10 @@ Staging* StarForest::acquire_staging(size_t ub, cudaStream_t stream) {
     // starts after that work completed (cudaStreamBeginCapture contract).
     return s.get();
   }
+  SFG_REQUIRE(capture_id(stream) == 0,
+              "first operation with a " + std::to_string(ub) +
+                  "-byte unit (or more operations in flight than staging slots) inside a CUDA graph "
+                  "capture: call prepare(unit) on the set-up forest before capturing");
   auto s = std::make_unique<Staging>();
   s->unit_bytes = ub;
   s->leaf_bytes = static_cast<size_t>(d.n_leafside) * ub;
@@ -711,6 +742,7 @@ Staging* StarForest::acquire_staging(size_t ub, cudaStream_t stream) {
     p2p_attach(*s);
   } else {
     if (s->leaf_bytes) SFG_CUDA(cudaMalloc(&s->leaf_stage, s->leaf_bytes));
+    if (s->leaf_bytes) SFG_CUDA(cudaMalloc(&s->leaf_reply, s->leaf_bytes));  // fetch-and-op replies
     if (s->root_bytes) SFG_CUDA(cudaMalloc(&s->root_stage, s->root_bytes));
   }
   SFG_CUDA(cudaMalloc(&s->digest, sizeof(unsigned long long)));

@@ -290,6 +290,82 @@ def g2l_halo(N, P: int, rank: int, dims=None, ghosts: bool = True,
     return GraphSpec(g.n_owned, local.size, local, rr, ro)
 
 
+def g2l_ghost_copies(g: G2L):
+    """Per-axis counts of how many neighbours ghost an owned point (star
+    stencil: a point on a block face with a neighbour across it is one ghost
+    leaf there). copies(x, y, z) = cx[x] + cy[y] + cz[z]."""
+    def axis(n, lo, hi):
+        c = np.zeros(n, np.int64)
+        c[0] += int(lo)
+        c[n - 1] += int(hi)
+        return c
+
+    return (axis(g.nx, g.bx > 0, g.bx < g.px - 1), axis(g.ny, g.by > 0, g.by < g.py - 1),
+            axis(g.nz, g.bz > 0, g.bz < g.pz - 1))
+
+
+def g2l_check(g: G2L, leaf, root_after) -> dict:
+    """Closed-form check of one Bcast(REPLACE) + Reduce(SUM) of the G2L forest
+    (``g2l_halo(..., interior=True)``) whose roots started as their local ids
+    0..n_owned-1 (float64), any P, every rank independently (torch tensors on
+    the device; no oracle, so it runs at the full 512^3 size):
+
+    * leaf box: interior = own ids; a face ghost = the id the neighbour gave
+      its boundary point; edges, corners and domain-boundary ghosts keep the
+      -1 the leaf array was filled with;
+    * roots: id + id (own interior leaf) + id per neighbour ghosting it =
+      id * (2 + copies), exact in float64 for ids < 2^50.
+    """
+    import torch
+
+    dev = leaf.device
+    f64 = torch.float64
+    nx, ny, nz = g.nx, g.ny, g.nz
+    ar = lambda n: torch.arange(n, dtype=f64, device=dev)  # noqa: E731
+    x, y, z = ar(nx), ar(ny), ar(nz)
+    want = torch.full((g.Z, g.Y, g.X), -1.0, dtype=f64, device=dev)
+    want[1:-1, 1:-1, 1:-1] = x[None, None, :] + nx * (y[None, :, None] + ny * z[:, None, None])
+    if g.bx > 0:  # neighbour's x = nxl-1 column
+        n = g.xs[g.bx - 1][1]
+        want[1:-1, 1:-1, 0] = (n - 1) + n * (y[None, :] + ny * z[:, None])
+    if g.bx < g.px - 1:
+        n = g.xs[g.bx + 1][1]
+        want[1:-1, 1:-1, -1] = n * (y[None, :] + ny * z[:, None])
+    if g.by > 0:
+        n = g.ys[g.by - 1][1]
+        want[1:-1, 0, 1:-1] = x[None, :] + nx * (n - 1) + nx * n * z[:, None]
+    if g.by < g.py - 1:
+        n = g.ys[g.by + 1][1]
+        want[1:-1, -1, 1:-1] = x[None, :] + nx * n * z[:, None]
+    if g.bz > 0:
+        n = g.zs[g.bz - 1][1]
+        want[0, 1:-1, 1:-1] = x[None, :] + nx * y[:, None] + nx * ny * (n - 1)
+    if g.bz < g.pz - 1:
+        want[-1, 1:-1, 1:-1] = x[None, :] + nx * y[:, None]
+    leaf_ok = bool(torch.equal(leaf.view(g.Z, g.Y, g.X), want))
+    del want
+    cx, cy, cz = (torch.from_numpy(c).to(dev) for c in g2l_ghost_copies(g))
+    copies = (cx[None, None, :] + cy[None, :, None] + cz[:, None, None]).reshape(-1)
+    ids = ar(g.n_owned)
+    root_ok = bool(torch.equal(root_after, ids * (2 + copies).to(f64)))
+    return {"leaf_ok": leaf_ok, "root_ok": root_ok}
+
+
+def g2l_reduce_expect(g: G2L, r):
+    """Roots after Bcast(REPLACE) + Reduce(SUM) of the G2L forest for ANY
+    float64 root values r: the fold r + r (own interior leaf) + r per ghost
+    copy, rounded after every addition in the reference order (all addends
+    are equal, so the order among ranks does not matter)."""
+    import torch
+
+    cx, cy, cz = (torch.from_numpy(c).to(r.device) for c in g2l_ghost_copies(g))
+    copies = (cx[None, None, :] + cy[None, :, None] + cz[:, None, None]).reshape(-1)
+    e = r + r
+    for t in range(1, 4):
+        e = torch.where(copies >= t, e + r, e)
+    return e
+
+
 # ------------------------------------------------------------------- config 3
 def laplacian27_ghosts(N: int, dims=(2, 2, 2), rank: int = 0, permute_seed: Optional[int] = None):
     """Ghost-column SF of a 27-point Laplacian on an N^3 grid partitioned in

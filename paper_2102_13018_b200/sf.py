@@ -414,6 +414,11 @@ class StarForest:
     def setup(self, alg: SetupAlg = SetupAlg.automatic) -> None:
         _check(_lib().sfg_sf_setup(self._h, int(alg)))
 
+    def prepare(self, unit: "Unit") -> None:
+        """Device plans + a staging slot for `unit`, built before a CUDA-graph
+        capture (SetUp does it for 8-byte units). Collective on p2p."""
+        _check(_lib().sfg_sf_prepare(self._h, int(unit.kind), unit.blocklen))
+
     def _info(self) -> L.sfg_sf_info:
         i = L.sfg_sf_info()
         _check(_lib().sfg_sf_get_info(self._h, C.byref(i)))

@@ -1,3 +1,3 @@
 O=gpurun_out; mkdir -p $O
 timeout 400 python bench_configs.py --config 1 > $O/cfg1_base.log 2>&1
-SFG_FREE_ORDER_ATOMICS=1 timeout 400 python bench_configs.py --config 1 > $O/cfg1_atomics.log 2>&1
+

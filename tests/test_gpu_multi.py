@@ -233,6 +233,30 @@ def test_p2p_needs_one_gpu_per_rank():
         sf.run_ranks(sf.CommConfig(nranks=2, backend="p2p"), body, devices=[0, 0])
 
 
+def _torchrun(n, port, args, timeout=900):
+    return subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port",
+                           str(port), *args], capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+
+
+@need2
+@pytest.mark.parametrize("backend", ["nccl", "p2p"])
+@pytest.mark.parametrize("n,dims", [(2, None), (4, None), (4, "2,2,1")])
+def test_config2_512_full_size_multi(backend, n, dims):
+    """BASELINE config 2 at full size (512^3) over 2 and 4 GPUs, one process
+    per GPU: every leaf and root after Bcast REPLACE + Reduce SUM equals its
+    closed form (graphs.g2l_check), and the float fold matches the sequential
+    reference order. 2,2,1 puts x-faces (stride-nx affine packs) in play, the
+    shape N=8's 2x2x2 grid has."""
+    if ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    port = 29540 + n + (0 if backend == "nccl" else 10) + (5 if dims else 0)
+    args = [os.path.join(ROOT, "tests", "mp_fullsize.py"), backend, "512"] + ([dims] if dims else [])
+    r = _torchrun(n, port, args)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "mp_fullsize ok" in r.stdout
+
+
 @need2
 @pytest.mark.parametrize("backend", ["nccl", "p2p"])
 def test_process_per_gpu_torchrun(backend):
