@@ -519,13 +519,16 @@ def ours(args, rank, world, local):
     # roots = their local ids, one Bcast REPLACE + Reduce SUM, closed form.
     ids = torch.arange(geo.n_owned, dtype=torch.float64, device="cuda")
     leaf.fill_(-1.0)
+    torch.cuda.synchronize()  # ids / leaf were written on the default stream
+    barrier()
     with torch.cuda.stream(stream):
         step_on(ids)
     torch.cuda.synchronize()
     chk = graphs.g2l_check(geo, leaf, ids)
     del ids
     nbad = allreduce(0.0 if (chk["leaf_ok"] and chk["root_ok"]) else 1.0, "sum")
-    check = {"result_ok": nbad == 0, "ranks_failed": int(nbad),
+    nleaf = allreduce(0.0 if chk["leaf_ok"] else 1.0, "sum")
+    check = {"result_ok": nbad == 0, "ranks_failed": int(nbad), "ranks_leaf_failed": int(nleaf),
              "what": "roots = local ids; Bcast REPLACE + Reduce SUM; every leaf of the ghosted box "
                      "and every root equal their closed form (id, neighbour's id, id*(2+ghost copies))"}
 

@@ -158,6 +158,56 @@ def timed_graph(ctx, fn, steps, warmup, reps=5):
     return ctx.vmax(statistics.median(per))
 
 
+def timed_graph_flushed(ctx, fn, steps=10, reps=5):
+    """Device time per call with a cold L2: a CUDA graph of `steps` x
+    [L2 read-flush, call] minus a graph of `steps` x [flush] (same stream),
+    median over `reps` replays, max over ranks. No host launch gap inside the
+    measurement (the eager per-call events include the Python/ctypes time it
+    takes to issue Begin/End after the flush)."""
+    torch = ctx.torch
+    flush_buf = torch.ones(64 << 20, dtype=torch.int32, device="cuda")
+    flush_out = torch.empty((), dtype=torch.int64, device="cuda")
+
+    def flush():
+        torch.sum(flush_buf, dim=0, dtype=torch.int64, out=flush_out)
+
+    with torch.cuda.stream(ctx.stream):
+        for _ in range(2):
+            flush()
+            fn()
+    torch.cuda.synchronize()
+    ctx.barrier()
+    gs = []
+    for with_op in (True, False):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=ctx.stream):
+            for _ in range(steps):
+                flush()
+                if with_op:
+                    fn()
+        gs.append(g)
+    torch.cuda.synchronize()
+    ctx.barrier()
+    t = {}
+    for name, g in zip(("op", "flush"), gs):
+        g.replay()
+        torch.cuda.synchronize()
+        per = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ctx.barrier()
+            with torch.cuda.stream(ctx.stream):
+                e0.record(ctx.stream)
+                g.replay()
+                e1.record(ctx.stream)
+            torch.cuda.synchronize()
+            per.append(e0.elapsed_time(e1) / steps)
+        t[name] = statistics.median(per)
+    ctx.barrier()
+    del gs
+    return ctx.vmax(t["op"] - t["flush"])
+
+
 def peak():
     try:
         return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
@@ -225,8 +275,12 @@ def config1(ctx, args):
 
         for name, fn in (("bcast_replace", bc), ("reduce_sum", rd)):
             ms, byts, rec = ctx.timed(fn, args.steps, args.warmup)
+            gms = timed_graph_flushed(ctx, fn)
             op_line(ctx, 1, name, ms, byts, rec, {"deterministic": det, "setup_s": setup_s,
-                                                   "L": L, "R": R, "dtype": "f64"})
+                                                   "L": L, "R": R, "dtype": "f64",
+                                                   "graph_us_per_op": gms * 1e3,
+                                                   "graph_GBps": byts / (gms * 1e-3) / 1e9,
+                                                   "graph_frac_hbm": byts / (gms * 1e-3) / 1e9 / peak()})
     if args.cpu and ctx.world == 1 and ctx.rank == 0:
         from oracle import ref
 
@@ -298,8 +352,12 @@ def config4(ctx, args):
 
             for name, fn in (("reduce_sum", rd), ("fetch_and_op_sum", fo)):
                 ms, byts, rec = ctx.timed(fn, args.steps, args.warmup)
+                gms = timed_graph_flushed(ctx, fn)
                 op_line(ctx, 4, name, ms, byts, rec, {"deterministic": det, "dtype": dt,
-                                                       "setup_s": setup_s, "L": L, "R": R})
+                                                       "setup_s": setup_s, "L": L, "R": R,
+                                                       "graph_us_per_op": gms * 1e3,
+                                                       "graph_GBps": byts / (gms * 1e-3) / 1e9,
+                                                       "graph_frac_hbm": byts / (gms * 1e-3) / 1e9 / peak()})
     if args.cpu and ctx.world == 1 and ctx.rank == 0:
         from oracle import ref
 
@@ -369,6 +427,18 @@ def config5(ctx, args):
         size *= 2
     emit(ctx, {"config": 5, "op": "pingpong_bcast+reduce_replace", "n_gpus": 2,
                "transport": ctx.transport, "rows": rows})
+    if args.cpu and ctx.rank == 0:
+        # the reference's own ping-pong (bench.cpp:24-100) on this box's host,
+        # 2 rank threads, sizes x4 from 8 B (its sweep step)
+        from oracle import ref
+
+        if ref.available():
+            import os as _os
+            cores = len(_os.sched_getaffinity(0)) if hasattr(_os, "sched_getaffinity") else _os.cpu_count()
+            rrows = ref.pingpong(8, min(args.max_bytes, 64 << 20), iters=20, warmup=3)
+            emit(ctx, {"config": 5, "op": "pingpong_bcast+reduce_replace", "impl": "reference_cpu",
+                       "cores": 2, "host_cores": cores, "rows": rrows,
+                       "what": "sf::pingpong (bench.cpp:24-100), threads backend, median/min half RTT"})
 
 
 # ------------------------------------------------------- config 3 consumer

@@ -170,6 +170,21 @@ def time_op(specs, opkind: str, dtype: str, op: str, steps: int, warmup: int = 1
     return {"setup_s": float(out[0]), "us_per_call": float(out[1])}
 
 
+def pingpong(min_bytes: int, max_bytes: int, iters: int = 50, warmup: int = 5) -> list[dict]:
+    """The reference's own 2-rank ping-pong benchmark (bench.cpp:24-100):
+    sizes x4 from min_bytes; half round trip median / min in microseconds."""
+    lib = _load()
+    if not getattr(lib, "_pingpong_typed", False):
+        lib.sfref_pingpong.argtypes = [C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_int]
+        lib._pingpong_typed = True
+    out = np.zeros(3 * 64, np.float64)
+    k = lib.sfref_pingpong(min_bytes, max_bytes, iters, warmup, out.ctypes.data, 64)
+    if k < 0:
+        raise RuntimeError(lib.sfref_last_error().decode())
+    return [{"bytes": int(out[3 * i]), "median_us": float(out[3 * i + 1]), "min_us": float(out[3 * i + 2])}
+            for i in range(k)]
+
+
 def spmv(nranks: int, rowptr, colind, vals, x, transpose: bool = False) -> np.ndarray:
     """The reference's distributed spmv / spmv_transpose (spmv.hpp:147-169)
     over `nranks` rank threads with contiguous layouts, as selfcheck.cpp's

@@ -18,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include "sf/bench.hpp"
 #include "sf/harness.hpp"
 #include "sf/rng.hpp"
 #include "sf/ops.hpp"
@@ -237,6 +238,33 @@ int sfref_time_op(int nranks, const int64_t* nroots, const int64_t* nleaves,
   } catch (const std::exception& e) {
     g_err = e.what();
     return 1;
+  }
+}
+
+// The reference's own ping-pong benchmark (bench.cpp:24-100, sf::pingpong):
+// sizes min_bytes, 4*min_bytes, ... <= max_bytes; per size out[3*k] = bytes,
+// out[3*k+1] = median half round trip (us), out[3*k+2] = min (us). Returns the
+// number of rows, -1 on error.
+int sfref_pingpong(int64_t min_bytes, int64_t max_bytes, int iters, int warmup, double* out, int cap) {
+  try {
+    sf::PingPongConfig cfg;
+    cfg.min_bytes = min_bytes;
+    cfg.max_bytes = max_bytes;
+    cfg.iters = iters;
+    cfg.warmup = warmup;
+    const auto rows = sf::pingpong(cfg);
+    int k = 0;
+    for (const auto& r : rows) {
+      if (k >= cap) break;
+      out[3 * k] = static_cast<double>(r.bytes);
+      out[3 * k + 1] = r.median_us;
+      out[3 * k + 2] = r.min_us;
+      ++k;
+    }
+    return k;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
   }
 }
 

@@ -548,7 +548,9 @@ __device__ __forceinline__ void wait_flags(const LaunchParams& P, uint32_t mask)
     const unsigned long long t0 = global_ns();
     for (uint32_t m = mask; m; m &= m - 1) {
       const FlagWait& w = P.waits[__ffs(m) - 1];
-      const unsigned long long need = *w.count + w.delta;
+      const long long want = static_cast<long long>(*w.count) + w.delta;
+      if (want <= 0) continue;
+      const unsigned long long need = static_cast<unsigned long long>(want);
       while (ld_acquire_sys(w.flag) < need) {
         __nanosleep(32);
         if (global_ns() - t0 > 30000000000ull) {
@@ -606,6 +608,125 @@ __device__ __forceinline__ void signal_segment_done(const DSeg& seg, int64_t nbl
   }
 }
 
+// ------------------------------------------------------------ LL128 (p2p)
+__device__ __forceinline__ void st_v2_volatile(unsigned long long* p, unsigned long long a,
+                                               unsigned long long b) {
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_v2_volatile(const unsigned long long* p, unsigned long long& a,
+                                               unsigned long long& b) {
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+
+// Message number of this CTA's segment: *counter + 1 (the counter advances
+// only after every CTA of the segment / launch has arrived).
+__device__ __forceinline__ unsigned long long ll_message(const unsigned long long* counter) {
+  __shared__ unsigned long long m;
+  __syncthreads();
+  if (threadIdx.x == 0) m = *counter + 1;
+  __syncthreads();
+  return m;
+}
+
+// Put: word w of the message = word (w % wpv) of vertex src[pat(w / wpv)];
+// lane l writes words 2j, 2j+1 (j = l % 8) of line 4*warp + l/8 of this
+// CTA's block; lane 7 of each line carries the flag m in word 15.
+__device__ __forceinline__ void run_put_ll(const DSeg& s, const LaunchParams& P, int64_t blk) {
+  const unsigned long long m = ll_message(s.sig_seq);
+  const auto* src = static_cast<const unsigned long long*>(P.bufs[s.src_buf]);
+  auto* dst = static_cast<unsigned long long*>(P.bufs[s.dst_buf]) + static_cast<int64_t>(m & 1) * s.ll_par;
+  const int64_t wpv = P.wpv;
+  const int64_t W = s.n * wpv;
+  const int64_t lines = (W + 14) / 15;
+  const int lane = threadIdx.x & 31;
+  const int j = lane & 7;
+  const int64_t L = blk * kLLLines + (threadIdx.x >> 5) * 4 + (lane >> 3);
+  if (L >= lines) return;
+  const int64_t w0 = L * 15 + 2 * j;
+  unsigned long long a = 0, b = m;
+  if (w0 < W) {
+    const int64_t i = w0 / wpv;
+    a = src[pat_index(s.src, i) * wpv + (w0 - i * wpv)];
+  }
+  if (j != 7 && w0 + 1 < W) {
+    const int64_t i = (w0 + 1) / wpv;
+    b = src[pat_index(s.src, i) * wpv + (w0 + 1 - i * wpv)];
+  }
+  st_v2_volatile(dst + (s.ll_line + L) * 16 + 2 * j, a, b);
+}
+
+// Receive: poll this warp's 4 lines until every flag is m, then apply each
+// data word's elements to dst[pat(vertex)] (op; REPLACE copies).
+template <class T, int OP>
+__device__ __forceinline__ void run_recv_ll(const DSeg& s, const LaunchParams& P, int64_t blk) {
+  const unsigned long long m = ll_message(s.sig_seq);
+  const auto* reg = static_cast<const unsigned long long*>(P.bufs[s.src_buf]) + static_cast<int64_t>(m & 1) * s.ll_par;
+  T* dst = static_cast<T*>(P.bufs[s.dst_buf]);
+  constexpr int kEpw = 8 / static_cast<int>(sizeof(T));  // elements per word
+  const int64_t wpv = P.wpv;
+  const int64_t W = s.n * wpv;
+  const int64_t lines = (W + 14) / 15;
+  const int lane = threadIdx.x & 31;
+  const int j = lane & 7;
+  const int64_t L = blk * kLLLines + (threadIdx.x >> 5) * 4 + (lane >> 3);
+  const bool live = L < lines;
+  if (__all_sync(0xffffffffu, !live)) return;
+  unsigned long long a = 0, b = 0;
+  const unsigned long long t0 = global_ns();
+  for (;;) {
+    if (live) ld_v2_volatile(reg + (s.ll_line + L) * 16 + 2 * j, a, b);
+    const unsigned long long f = __shfl_sync(0xffffffffu, b, (lane & ~7) | 7);
+    if (__all_sync(0xffffffffu, !live || f == m)) break;
+    __nanosleep(20);
+    if (global_ns() - t0 > 30000000000ull) {
+      if (lane == 0) printf("sfgpu p2p: LL128 line never arrived (message %llu)\n", m);
+      __trap();
+    }
+  }
+  if (!live) return;
+  const int64_t bl = P.bl;
+  const int64_t w0 = L * 15 + 2 * j;
+  const int nw = j == 7 ? 1 : 2;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int64_t w = w0 + q;
+    if (q >= nw || w >= W) break;
+    const unsigned long long word = q == 0 ? a : b;
+#pragma unroll
+    for (int t = 0; t < kEpw; ++t) {
+      const int64_t e = w * kEpw + t;  // element index in the message
+      const int64_t i = e / bl;
+      const int64_t k = e - i * bl;
+      T v;
+      const unsigned long long part = kEpw == 1 ? word : (word >> (32 * t));
+      if constexpr (sizeof(T) == 8) {
+        v = *reinterpret_cast<const T*>(&part);
+      } else if constexpr (sizeof(T) == 4) {
+        const uint32_t lo = static_cast<uint32_t>(part);
+        v = *reinterpret_cast<const T*>(&lo);
+      } else {
+        v = T();
+      }
+      T* d = dst + pat_index(s.dst, i) * bl + k;
+      if constexpr (OP == OP_REPLACE)
+        *d = v;
+      else
+        *d = apply_op<T, OP>(*d, v);
+    }
+  }
+}
+
+// LL128 put completion: no flag (every line carries its own); the last CTA
+// of the segment advances the channel's message counter.
+__device__ __forceinline__ void count_put_ll(const DSeg& seg, int64_t nblk) {
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  if (static_cast<int64_t>(cta_arrive(seg.sig_count)) + 1 == nblk) {
+    *seg.sig_count = 0u;
+    *seg.sig_seq = *seg.sig_seq + 1;
+  }
+}
+
 // FULL = the launch contains root-sorted (CSR) or fetch segments. Pair-only
 // launches (every pack, unpack and structured local scatter) get their own
 // instantiation so the CSR paths do not raise their register allocation.
@@ -631,6 +752,17 @@ __global__ void __launch_bounds__(kThreads, FULL ? 3 : 4) segments_kernel(const 
           run_pair<T, OP>(seg, P, blk);
       }
       break;
+    case SEG_PUT_LL:
+      if constexpr (sizeof(T) >= 4) run_put_ll(seg, P, blk);
+      break;
+    case SEG_RECV_LL:
+      if constexpr (sizeof(T) >= 4) {
+        if (seg.replace)
+          run_recv_ll<T, OP_REPLACE>(seg, P, blk);
+        else
+          run_recv_ll<T, OP>(seg, P, blk);
+      }
+      break;
     case SEG_CSR_FOLD:
       if constexpr (OP != OP_REPLACE && FULL) {
         if (seg.csr_warp)
@@ -650,7 +782,10 @@ __global__ void __launch_bounds__(kThreads, FULL ? 3 : 4) segments_kernel(const 
     default:
       break;
   }
-  if (seg.sig_flag != nullptr) signal_segment_done(seg, P.block_start[s + 1] - P.block_start[s]);
+  if (seg.type == SEG_PUT_LL)
+    count_put_ll(seg, P.block_start[s + 1] - P.block_start[s]);
+  else if (seg.sig_flag != nullptr)
+    signal_segment_done(seg, P.block_start[s + 1] - P.block_start[s]);
   if (P.ndone > 0) signal_launch_done(P);
 }
 
@@ -792,8 +927,10 @@ int launch_segments(LaunchParams& p, ElemType t, int op, cudaStream_t stream) {
     p.seg[n] = p.seg[s];
     p.block_start[n] = blocks;
     const bool csr = p.seg[s].type == SEG_CSR_FOLD || p.seg[s].type == SEG_CSR_FETCH;
+    const bool ll = p.seg[s].type == SEG_PUT_LL || p.seg[s].type == SEG_RECV_LL;
     const int64_t per_block = !csr ? kThreads * kItems : p.seg[n].csr_warp ? kThreads / 32 : kThreads;
     int64_t nb = (items + per_block - 1) / per_block;
+    if (ll) nb = ((p.seg[s].n * p.wpv + 14) / 15 + kLLLines - 1) / kLLLines;
     if (csr && p.seg[n].csr_np > 1) {
       // Piece-major walk: every CTA of the segment must be resident at once.
       const int64_t res = resident_ctas(t, op);

@@ -53,7 +53,20 @@ enum SegType : int32_t {
   SEG_PAIR = 0,
   SEG_CSR_FOLD = 2,
   SEG_CSR_FETCH = 3,
+  SEG_PUT_LL = 4,   // p2p: src pattern -> peer's LL128 region (lines + flag)
+  SEG_RECV_LL = 5,  // p2p: my LL128 region -> dst pattern (op), polling lines
 };
+
+// LL128 messages (p2p backend, units that are a multiple of 8 bytes): a
+// message of W 8-byte words travels as ceil(W/15) 128-byte lines; words
+// 0..14 of a line carry data, word 15 the message number m. A warp writes a
+// line with ONE 16-byte store per lane (8 lanes per line), which NVLink
+// delivers as one transaction, so a receiver that sees the flag m in a line
+// sees the whole line: no fence, no completion flag, and the unpack of a
+// line starts as soon as it lands (NCCL's LL128 protocol). Each receive
+// region holds two messages per channel (parity m & 1), so a put waits only
+// for the acknowledgement of message m-2, which is long done.
+constexpr int kLLLines = 32;  // lines per CTA (4 per warp)
 
 // Buffer slots a segment can address; filled per call.
 enum BufId : int32_t {
@@ -64,8 +77,9 @@ enum BufId : int32_t {
   BUF_LEAFUPDATE = 4,  // fetch-and-op leafupdate
   BUF_LEAF_REPLY = 5,  // fetch-and-op reply staging on the leaf side
   BUF_SRC_RO = 6,      // read-only source alias (leafdata for reduce/fetch)
-  BUF_PEER0 = 8,       // p2p transport: peer r's mapped staging slot is BUF_PEER0 + r
-  BUF_COUNT = 8 + 16
+  BUF_LL0 = 7,         // p2p LL128: my receive regions 0 (leaf), 1 (root), 2 (reply)
+  BUF_PEER0 = 10,      // p2p transport: a put's peer region is BUF_PEER0 + k
+  BUF_COUNT = 10 + 16
 };
 constexpr int kMaxPeers = BUF_COUNT - BUF_PEER0;
 
@@ -122,13 +136,18 @@ struct DSeg {
   unsigned int* sig_count = nullptr;
   unsigned long long* sig_flag = nullptr;
   unsigned long long* sig_seq = nullptr;
+  // LL128 segments: the group's first line in the region and the words per
+  // parity buffer of the region; sig_seq is the channel's message counter
+  // (sent for puts, recvd for receives: message m = *sig_seq + 1).
+  int64_t ll_line = 0;
+  int64_t ll_par = 0;
 };
 
 // Wait until *flag >= *count + delta (count: a local message counter).
 struct FlagWait {
   const unsigned long long* flag = nullptr;
   const unsigned long long* count = nullptr;
-  unsigned long long delta = 0;
+  long long delta = 0;  // wait for *flag >= *count + delta (nothing when <= 0)
 };
 
 constexpr int kMaxSegs = 12;
@@ -155,6 +174,7 @@ struct LaunchParams {
   void* bufs[BUF_COUNT];
   int64_t bl = 1;  // elements per vertex
   FastDiv bldiv;
+  int64_t wpv = 1;  // LL128: 8-byte words per vertex (unit bytes / 8)
   int nseg = 0;
   // p2p: flags segments wait on (bit i of DSeg::wait_mask = waits[i]) and the
   // acknowledgements the launch raises once all its CTAs are done (advance

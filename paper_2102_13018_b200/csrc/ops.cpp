@@ -252,6 +252,22 @@ struct Launch {
     items.back().remote_put = remote;
   }
 
+  // LL128 put into a peer's region (see kernels.hpp): credit wait `wait`,
+  // the channel's message counter `seq` (sent), its CTA counter `sig_count`.
+  void add_put_ll(const DPat& src, int sbuf, void* region, int64_t line, int64_t par, int64_t n, int wait,
+                  unsigned int* sig_count, unsigned long long* seq, bool remote, int64_t src_distinct = -1) {
+    DSeg s = pair_seg(src, sbuf, contig(0), BUF_PEER0, n, true);
+    s.type = SEG_PUT_LL;
+    s.run = 0;
+    s.ll_line = line;
+    s.ll_par = par;
+    s.sig_count = sig_count;
+    s.sig_seq = seq;
+    add(s, 0, src_distinct, -1, {wait});
+    items.back().peer = region;
+    items.back().remote_put = remote;
+  }
+
   void run(const Unit& u, ReduceOp op, cudaStream_t st) {
     if (items.empty()) return;
     ElemType t;
@@ -303,6 +319,7 @@ struct Launch {
       LaunchParams p{};
       std::copy(bufs, bufs + BUF_PEER0, p.bufs);
       p.bl = bl;
+      p.wpv = static_cast<int64_t>(u.bytes() / 8);
       p.shuf = shuffle;
       std::vector<int> wmap(waits.size(), -1);
       int nw = 0, npeer = 0;
@@ -377,7 +394,9 @@ struct Launch {
       const double ds = static_cast<double>(it.distinct_src);
       const double dd = static_cast<double>(it.distinct_dst);
       switch (g.type) {
-        case SEG_PAIR: b += ds * ub + dd * ub * (g.replace ? 1.0 : 2.0) + idx; break;
+        case SEG_PAIR:
+        case SEG_RECV_LL: b += ds * ub + dd * ub * (g.replace ? 1.0 : 2.0) + idx; break;
+        case SEG_PUT_LL: b += ds * ub + n * ub * 128.0 / 120.0 + idx; break;
         case SEG_CSR_FOLD:
         case SEG_CSR_FETCH: {
           const double e = static_cast<double>(it.entries);
@@ -400,6 +419,8 @@ void set_bufs(Launch& L, const OpHandle& h, void* root, void* leaf, const void* 
     L.bufs[BUF_LEAF_REPLY] = h.stg->leaf_reply;
   }
   L.bufs[BUF_LEAFUPDATE] = h.leafupdate;
+  if (h.stg && h.stg->ll)
+    for (int r = 0; r < 3; ++r) L.bufs[BUF_LL0 + r] = h.stg->ll_region[r];
 }
 
 uint64_t data_tag(uint64_t opid) { return opid * 2; }
@@ -646,6 +667,62 @@ void add_acks(OpHandle& h, Launch& L, const std::vector<DevPlan::Seg>& groups, i
     L.add_done(s.peer_free_flag(region, g.rank, me), s.recvd(region, g.rank), s.done_count);
 }
 
+// ----------------------------------------------------- LL128 (p2p) phases
+// Slots whose unit is whole 8-byte words use the LL128 protocol (kernels.hpp):
+// puts carry a flag in every 128-byte line, receives poll the lines and
+// unpack as they land, two messages per channel in flight.
+bool use_ll(const OpHandle& h) { return use_p2p(h) && h.stg->ll; }
+
+// LL128 puts of `groups` (each group's pattern over sbuf, or its contiguous
+// range of the plain root stage when !use_pat) into the peers' `region`.
+void add_puts_ll(OpHandle& h, Launch& L, const std::vector<DevPlan::Seg>& groups, bool use_pat, int sbuf,
+                 int region) {
+  Staging& s = *h.stg;
+  const int me = h.sf->comm().rank();
+  const size_t ub = h.unit.bytes();
+  for (const auto& g : groups) {
+    const PeerSlot& ps = s.peers[static_cast<size_t>(g.rank)];
+    char* base = ps.base + (region == 0 ? 0 : region == 1 ? ps.root_at : ps.reply_at);
+    const int64_t line = region == 1 ? ps.root_line : ps.leaf_line;
+    SFG_REQUIRE(line >= 0, "p2p: peer slot has no group for this rank");
+    // message m goes to parity m & 1: the peer consumed message m-2 there
+    const int w = L.add_wait(s.free_flag(region, g.rank), s.sent(region, g.rank), -1);
+    L.add_put_ll(use_pat ? g.pat : contig(g.stage_off), sbuf, base, line, ps.par[region], g.n, w,
+                 s.seg_count(region, g.rank), s.sent(region, g.rank), g.rank != me,
+                 use_pat ? g.distinct : -1);
+    if (g.rank != me) counters().bytes_sent += static_cast<uint64_t>(g.n) * ub;
+    counters().pack_elided++;  // the put gathers straight from the caller's buffer
+  }
+}
+
+// LL128 receives of the next message of each group from my `region` into
+// dpat(group) of dbuf (op, or REPLACE when `replace`); the launch
+// acknowledges the messages once all its CTAs are done.
+void add_recvs_ll(OpHandle& h, Launch& L, const std::vector<DevPlan::Seg>& groups, int region,
+                  const std::function<DPat(const DevPlan::Seg&)>& dpat, int dbuf, bool replace) {
+  Staging& s = *h.stg;
+  const int me = h.sf->comm().rank();
+  const auto& lines = region == 1 ? s.lg_line : s.rg_line;
+  for (size_t k = 0; k < groups.size(); ++k) {
+    const auto& g = groups[k];
+    DSeg sg = pair_seg(contig(0), BUF_LL0 + region, dpat(g), dbuf, g.n, replace);
+    sg.type = SEG_RECV_LL;
+    sg.run = 0;
+    sg.ll_line = lines[k];
+    sg.ll_par = s.ll_par[region];
+    sg.sig_seq = s.recvd(region, g.rank);
+    L.add(sg, 0, -1, g.distinct);
+    L.add_done(s.peer_free_flag(region, g.rank, me), s.recvd(region, g.rank), s.done_count);
+    counters().bytes_recv += static_cast<uint64_t>(g.n) * h.unit.bytes();
+    counters().unpack_copies++;
+  }
+}
+
+bool has_self_group(const OpHandle& h, const std::vector<DevPlan::Seg>& groups) {
+  const int me = h.sf->comm().rank();
+  return std::any_of(groups.begin(), groups.end(), [me](const DevPlan::Seg& g) { return g.rank == me; });
+}
+
 // ---------------------------------------------------------- root -> leaf
 void begin_root_to_leaf(OpHandle& h) {
   StarForest& sf = *h.sf;
@@ -655,6 +732,24 @@ void begin_root_to_leaf(OpHandle& h) {
   Launch pack, local;
   set_bufs(pack, h, const_cast<void*>(h.src), h.dst, h.src);
   set_bufs(local, h, const_cast<void*>(h.src), h.dst, h.src);
+  if (use_ll(h)) {
+    add_puts_ll(h, pack, d.lg, true, BUF_ROOT, 0);
+    if (d.has_self)
+      local.add(pair_seg(d.self_root, BUF_ROOT, d.self_leaf, BUF_LEAF, d.n_self, replace), 0,
+                d.self_root_distinct);
+    // The receives join the put launch behind the puts and the local part
+    // (leafdata belongs to the operation between Begin and End); a self
+    // group (force_remote) receives in End instead.
+    h.fused_unpack = false;
+    const bool self_group = has_self_group(h, d.rg);
+    auto fuse = [&](Launch& L) {
+      if (self_group) return;
+      add_recvs_ll(h, L, d.rg, 0, [](const DevPlan::Seg& g) { return g.pat; }, BUF_LEAF, replace);
+      h.fused_unpack = true;
+    };
+    p2p_begin(h, pack, local, fuse);
+    return;
+  }
   if (use_p2p(h)) {
     add_puts(h, pack, d.lg, true, BUF_ROOT, 0);
     if (d.has_self)
@@ -730,6 +825,12 @@ void end_root_to_leaf(OpHandle& h) {
     p2p_join(h);
     return;
   }
+  if (use_ll(h)) {
+    add_recvs_ll(h, L, d.rg, 0, [](const DevPlan::Seg& g) { return g.pat; }, BUF_LEAF, replace);
+    L.run(h.unit, h.op, h.forked ? c.comm_stream() : h.stream);
+    p2p_join(h);
+    return;
+  }
   if (use_p2p(h)) {
     const auto bits = add_receives(h, L, d.rg, 0, true);
     for (size_t k = 0; k < d.rg.size(); ++k) {
@@ -770,7 +871,10 @@ void begin_leaf_to_root(OpHandle& h) {
   const bool p2p = use_p2p(h);
 
   std::vector<XferOp> sends;
-  if (p2p) {
+  const bool ll = use_ll(h);
+  if (ll) {
+    add_puts_ll(h, pack, d.rg, true, BUF_LEAF, 1);
+  } else if (p2p) {
     add_puts(h, pack, d.rg, true, BUF_LEAF, 1);
   } else {
     for (const auto& g : d.rg) {
@@ -797,6 +901,20 @@ void begin_leaf_to_root(OpHandle& h) {
   h.coupled_split = split_coupled(sf, h);
   if (h.coupled_split)
     for (auto& it : local.items) it.seg.skip_dst = d.coupled_bits;
+  if (ll) {
+    // incoming contributions are copied out of the LL lines into the plain
+    // root stage in the put launch (acknowledged there); End folds them
+    const bool self_group = has_self_group(h, d.lg);
+    h.fused_unpack = false;
+    auto fuse = [&](Launch& L) {
+      if (self_group) return;
+      add_recvs_ll(h, L, d.lg, 1, [](const DevPlan::Seg& g) { return contig(g.stage_off); },
+                   BUF_ROOT_STAGE, true);
+      h.fused_unpack = true;
+    };
+    p2p_begin(h, pack, local, fuse);
+    return;
+  }
   if (p2p) {
     p2p_begin(h, pack, local);
     return;
@@ -825,10 +943,20 @@ void end_leaf_to_root(OpHandle& h) {
   std::vector<int> bits;
   auto wait_k = [&bits](size_t k) { return bits.empty() ? std::vector<int>{} : std::vector<int>{bits[k]}; };
   Comm& c = sf.comm();
+  const bool ll = use_ll(h);
+  if (ll && !h.fused_unpack) {
+    // self group (force_remote): copy the LL messages out here, behind Begin
+    Launch R;
+    R.tag = tag_of(h, 1);
+    set_bufs(R, h, h.dst, const_cast<void*>(h.src), h.src);
+    add_recvs_ll(h, R, d.lg, 1, [](const DevPlan::Seg& g) { return contig(g.stage_off); }, BUF_ROOT_STAGE,
+                 true);
+    R.run(h.unit, ReduceOp::replace, h.forked ? c.comm_stream() : h.stream);
+  }
   if (h.coupled_split) {
     // Whole fold of the coupled roots, concurrent with Begin's local part.
     const bool p2p = use_p2p(h);
-    if (p2p) bits = add_receives(h, L, d.lg, 1, true);
+    if (p2p && !ll) bits = add_receives(h, L, d.lg, 1, true);
     DSeg s = csr_seg(d, CsrRange::remote_only, SEG_CSR_FOLD, exact_seq(h, det), h.unit.bytes());
     s.csr_lo = d.ccsr_lo;
     s.csr_hi = d.ccsr_hi;
@@ -849,7 +977,7 @@ void end_leaf_to_root(OpHandle& h) {
   }
   if (use_p2p(h)) {
     p2p_join(h);
-    bits = add_receives(h, L, d.lg, 1, true);
+    if (!ll) bits = add_receives(h, L, d.lg, 1, true);
   } else {
     end_wait(h, data_tag(h.opid), h.recvs);
   }
@@ -881,6 +1009,21 @@ void begin_fetch(OpHandle& h) {
   const size_t ub = h.unit.bytes();
   Launch pack, local;
   set_bufs(pack, h, h.dst, const_cast<void*>(h.src), h.src);
+  if (use_ll(h)) {
+    // requests: LL puts + the copy of the incoming ones into the plain root
+    // stage (where End fetches in place and the replies start from)
+    add_puts_ll(h, pack, d.rg, true, BUF_LEAF, 1);
+    h.fused_unpack = false;
+    const bool self_group = has_self_group(h, d.lg);
+    auto fuse = [&](Launch& L) {
+      if (self_group) return;
+      add_recvs_ll(h, L, d.lg, 1, [](const DevPlan::Seg& g) { return contig(g.stage_off); },
+                   BUF_ROOT_STAGE, true);
+      h.fused_unpack = true;
+    };
+    p2p_begin(h, pack, local, fuse);
+    return;
+  }
   if (use_p2p(h)) {
     add_puts(h, pack, d.rg, true, BUF_LEAF, 1);
     p2p_begin(h, pack, local);
@@ -914,7 +1057,18 @@ void end_fetch(OpHandle& h) {
   L.tag = "fetch_end";
   set_bufs(L, h, h.dst, const_cast<void*>(h.src), h.src);
   std::vector<int> bits;
-  if (p2p) {
+  const bool ll = use_ll(h);
+  if (ll) {
+    if (!h.fused_unpack) {
+      Launch R;
+      R.tag = "fetch_end";
+      set_bufs(R, h, h.dst, const_cast<void*>(h.src), h.src);
+      add_recvs_ll(h, R, d.lg, 1, [](const DevPlan::Seg& g) { return contig(g.stage_off); }, BUF_ROOT_STAGE,
+                   true);
+      R.run(h.unit, ReduceOp::replace, h.forked ? c.comm_stream() : h.stream);
+    }
+    p2p_join(h);
+  } else if (p2p) {
     p2p_join(h);
     // Consumed (acknowledged) only after the replies have been read out of
     // the root stage below.
@@ -947,6 +1101,26 @@ void end_fetch(OpHandle& h) {
   L.run(h.unit, h.op, h.stream);
 
   // Replies travel back in place (ops.cpp:559-561), then land in leafupdate.
+  if (ll) {
+    // reply puts from the plain root stage and the receives of my replies
+    // into leafupdate, one launch (a self group receives in a second one)
+    Launch R;
+    R.tag = "fetch_replies";
+    set_bufs(R, h, h.dst, const_cast<void*>(h.src), h.src);
+    add_puts_ll(h, R, d.lg, false, BUF_ROOT_STAGE, 2);
+    auto upd = [](const DevPlan::Seg& g) { return g.pat; };
+    const bool self_group = has_self_group(h, d.rg);
+    if (!self_group) add_recvs_ll(h, R, d.rg, 2, upd, BUF_LEAFUPDATE, true);
+    R.run(h.unit, ReduceOp::replace, h.stream);
+    if (self_group) {
+      Launch U;
+      U.tag = "fetch_end_replies";
+      set_bufs(U, h, h.dst, const_cast<void*>(h.src), h.src);
+      add_recvs_ll(h, U, d.rg, 2, upd, BUF_LEAFUPDATE, true);
+      U.run(h.unit, ReduceOp::replace, h.stream);
+    }
+    return;
+  }
   if (p2p) {
     Launch R;
     R.tag = "fetch_replies";

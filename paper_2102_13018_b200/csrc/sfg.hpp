@@ -405,6 +405,10 @@ struct PeerSlot {
   size_t root_at = 0, reply_at = 0, flags_at = 0;  // byte offsets inside the slot
   int64_t leaf_off = -1;  // peer's leaf-stage vertex offset of my group (its rg)
   int64_t root_off = -1;  // peer's root-stage vertex offset of my group (its lg)
+  // LL128 slots: my group's first line in the peer's leaf / root (and reply)
+  // regions, and the peer's words per parity buffer of each region
+  int64_t leaf_line = -1, root_line = -1;
+  int64_t par[3] = {0, 0, 0};
 };
 
 struct Staging {
@@ -434,6 +438,14 @@ struct Staging {
   // The kernels advance the counters themselves — no host bookkeeping — so
   // operations can be captured into a CUDA graph and replayed.
   void* slot_mem = nullptr;
+  // LL128 protocol (unit bytes a multiple of 8): the three regions receive
+  // LL128 lines, two messages per channel; incoming root-side messages are
+  // copied into the plain root_stage (its own allocation) for the folds.
+  bool ll = false;
+  void* ll_region[3] = {nullptr, nullptr, nullptr};
+  int64_t ll_par[3] = {0, 0, 0};        // words per parity buffer of each region
+  std::vector<int64_t> rg_line, lg_line;  // first line of each of my groups (rg: regions 0/2, lg: region 1)
+  void* plain_root = nullptr;
   unsigned long long* flags = nullptr;
   unsigned int* seg_counts = nullptr;
   unsigned int* done_count = nullptr;

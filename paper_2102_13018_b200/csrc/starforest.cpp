@@ -71,6 +71,7 @@ Staging::~Staging() {
   }
   for (auto& p : peers)
     if (p.ipc && p.base) cudaIpcCloseMemHandle(p.base);
+  if (plain_root) cudaFree(plain_root);
   if (slot_mem) {
     cudaFree(slot_mem);
   } else {
@@ -315,7 +316,14 @@ void StarForest::setup(SetupAlg alg) {
 void StarForest::prepare_default() {
   if (!comm_->has_device()) return;
   comm_->bind_device();
-  prepare(8);
+  try {
+    prepare(8);
+  } catch (const CudaError&) {
+    throw;
+  } catch (const Error&) {
+    // A forest the device plans cannot hold (indices beyond int32): SetUp
+    // still succeeds, as in the reference; the first operation reports it.
+  }
 }
 
 const std::vector<Group>& StarForest::root_groups() const {

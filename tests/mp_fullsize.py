@@ -35,6 +35,8 @@ def main():
     ids = torch.arange(geo.n_owned, dtype=torch.float64, device="cuda")
     leaf = torch.full((geo.n_local,), -1.0, dtype=torch.float64, device="cuda")
     st = torch.cuda.Stream()
+    torch.cuda.synchronize()  # ids / leaf were written on the default stream
+    dist.barrier()
     with torch.cuda.stream(st):
         sf.bcast_end(sf.bcast_begin(f, u, ids, leaf, sf.ReduceOp.replace, st))
         sf.reduce_end(sf.reduce_begin(f, u, leaf, ids, sf.ReduceOp.sum, st))
@@ -44,6 +46,8 @@ def main():
     # root with its copies, rounded per addition.
     r0 = torch.rand(geo.n_owned, dtype=torch.float64, device="cuda")
     r = r0.clone()
+    torch.cuda.synchronize()
+    dist.barrier()
     with torch.cuda.stream(st):
         sf.bcast_end(sf.bcast_begin(f, u, r, leaf, sf.ReduceOp.replace, st))
         sf.reduce_end(sf.reduce_begin(f, u, leaf, r, sf.ReduceOp.sum, st))
