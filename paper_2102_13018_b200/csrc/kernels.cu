@@ -534,6 +534,14 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// LL128 acknowledgements: the acknowledged LL lines were all read (their
+// values consumed) before the last CTA arrived, and a peer only reuses that
+// parity two messages later, so no system fence is needed (a MEMBAR.SYS at
+// the end of every receiving launch would lengthen each exchange).
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -588,7 +596,10 @@ __device__ __forceinline__ void signal_launch_done(const LaunchParams& P) {
     for (int i = 0; i < P.ndone; ++i) {
       const unsigned long long v = *P.done_seq[i] + 1;
       *P.done_seq[i] = v;
-      st_release_sys(P.done_flag[i], v);
+      if (P.done_relaxed)
+        st_relaxed_sys(P.done_flag[i], v);
+      else
+        st_release_sys(P.done_flag[i], v);
     }
   }
 }
@@ -628,9 +639,11 @@ __device__ __forceinline__ unsigned long long ll_message(const unsigned long lon
   return m;
 }
 
-// Put: word w of the message = word (w % wpv) of vertex src[pat(w / wpv)];
-// lane l writes words 2j, 2j+1 (j = l % 8) of line 4*warp + l/8 of this
-// CTA's block; lane 7 of each line carries the flag m in word 15.
+// Put: word w of the message = word (w % wpv) of vertex src[pat(w / wpv)].
+// A CTA covers kLLLines lines: warp q, iteration u, lane l writes words
+// 2j, 2j+1 (j = l % 8) of line 4*(kLLIters*q + u) + l/8; lane 7 of each line
+// carries the flag m in word 15. All source loads of a thread are issued
+// before its stores.
 __device__ __forceinline__ void run_put_ll(const DSeg& s, const LaunchParams& P, int64_t blk) {
   const unsigned long long m = ll_message(s.sig_seq);
   const auto* src = static_cast<const unsigned long long*>(P.bufs[s.src_buf]);
@@ -640,22 +653,31 @@ __device__ __forceinline__ void run_put_ll(const DSeg& s, const LaunchParams& P,
   const int64_t lines = (W + 14) / 15;
   const int lane = threadIdx.x & 31;
   const int j = lane & 7;
-  const int64_t L = blk * kLLLines + (threadIdx.x >> 5) * 4 + (lane >> 3);
-  if (L >= lines) return;
-  const int64_t w0 = L * 15 + 2 * j;
-  unsigned long long a = 0, b = m;
-  if (w0 < W) {
-    const int64_t i = w0 / wpv;
-    a = src[pat_index(s.src, i) * wpv + (w0 - i * wpv)];
+  const int64_t L0 = blk * kLLLines + (threadIdx.x >> 5) * (4 * kLLIters) + (lane >> 3);
+  unsigned long long a[kLLIters], b[kLLIters];
+#pragma unroll
+  for (int u = 0; u < kLLIters; ++u) {
+    const int64_t L = L0 + 4 * u;
+    const int64_t w0 = L * 15 + 2 * j;
+    a[u] = 0;
+    b[u] = m;
+    if (L < lines && w0 < W) {
+      const int64_t i = w0 / wpv;
+      a[u] = src[pat_index(s.src, i) * wpv + (w0 - i * wpv)];
+    }
+    if (L < lines && j != 7 && w0 + 1 < W) {
+      const int64_t i = (w0 + 1) / wpv;
+      b[u] = src[pat_index(s.src, i) * wpv + (w0 + 1 - i * wpv)];
+    }
   }
-  if (j != 7 && w0 + 1 < W) {
-    const int64_t i = (w0 + 1) / wpv;
-    b = src[pat_index(s.src, i) * wpv + (w0 + 1 - i * wpv)];
+#pragma unroll
+  for (int u = 0; u < kLLIters; ++u) {
+    const int64_t L = L0 + 4 * u;
+    if (L < lines) st_v2_volatile(dst + (s.ll_line + L) * 16 + 2 * j, a[u], b[u]);
   }
-  st_v2_volatile(dst + (s.ll_line + L) * 16 + 2 * j, a, b);
 }
 
-// Receive: poll this warp's 4 lines until every flag is m, then apply each
+// Receive: poll this thread's lines until every flag is m, then apply each
 // data word's elements to dst[pat(vertex)] (op; REPLACE copies).
 template <class T, int OP>
 __device__ __forceinline__ void run_recv_ll(const DSeg& s, const LaunchParams& P, int64_t blk) {
@@ -668,50 +690,57 @@ __device__ __forceinline__ void run_recv_ll(const DSeg& s, const LaunchParams& P
   const int64_t lines = (W + 14) / 15;
   const int lane = threadIdx.x & 31;
   const int j = lane & 7;
-  const int64_t L = blk * kLLLines + (threadIdx.x >> 5) * 4 + (lane >> 3);
-  const bool live = L < lines;
-  if (__all_sync(0xffffffffu, !live)) return;
-  unsigned long long a = 0, b = 0;
+  const int64_t L0 = blk * kLLLines + (threadIdx.x >> 5) * (4 * kLLIters) + (lane >> 3);
+  if (__all_sync(0xffffffffu, L0 >= lines)) return;
+  unsigned long long a[kLLIters], b[kLLIters];
   const unsigned long long t0 = global_ns();
   for (;;) {
-    if (live) ld_v2_volatile(reg + (s.ll_line + L) * 16 + 2 * j, a, b);
-    const unsigned long long f = __shfl_sync(0xffffffffu, b, (lane & ~7) | 7);
-    if (__all_sync(0xffffffffu, !live || f == m)) break;
+    bool ok = true;
+#pragma unroll
+    for (int u = 0; u < kLLIters; ++u) {
+      const int64_t L = L0 + 4 * u;
+      a[u] = 0;
+      b[u] = m;
+      if (L < lines) ld_v2_volatile(reg + (s.ll_line + L) * 16 + 2 * j, a[u], b[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kLLIters; ++u) ok = ok && __shfl_sync(0xffffffffu, b[u], (lane & ~7) | 7) == m;
+    if (__all_sync(0xffffffffu, ok)) break;
     __nanosleep(20);
     if (global_ns() - t0 > 30000000000ull) {
       if (lane == 0) printf("sfgpu p2p: LL128 line never arrived (message %llu)\n", m);
       __trap();
     }
   }
-  if (!live) return;
   const int64_t bl = P.bl;
-  const int64_t w0 = L * 15 + 2 * j;
-  const int nw = j == 7 ? 1 : 2;
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int64_t w = w0 + q;
-    if (q >= nw || w >= W) break;
-    const unsigned long long word = q == 0 ? a : b;
+  for (int u = 0; u < kLLIters; ++u) {
+    const int64_t L = L0 + 4 * u;
+    if (L >= lines) break;
+    const int64_t w0 = L * 15 + 2 * j;
 #pragma unroll
-    for (int t = 0; t < kEpw; ++t) {
-      const int64_t e = w * kEpw + t;  // element index in the message
-      const int64_t i = e / bl;
-      const int64_t k = e - i * bl;
-      T v;
-      const unsigned long long part = kEpw == 1 ? word : (word >> (32 * t));
-      if constexpr (sizeof(T) == 8) {
-        v = *reinterpret_cast<const T*>(&part);
-      } else if constexpr (sizeof(T) == 4) {
-        const uint32_t lo = static_cast<uint32_t>(part);
-        v = *reinterpret_cast<const T*>(&lo);
-      } else {
-        v = T();
+    for (int q = 0; q < 2; ++q) {
+      const int64_t w = w0 + q;
+      if ((q == 1 && j == 7) || w >= W) break;
+      const unsigned long long word = q == 0 ? a[u] : b[u];
+#pragma unroll
+      for (int t = 0; t < kEpw; ++t) {
+        const int64_t e = w * kEpw + t;  // element index in the message
+        const int64_t i = e / bl;
+        const int64_t k = e - i * bl;
+        T v;
+        if constexpr (sizeof(T) == 8) {
+          v = *reinterpret_cast<const T*>(&word);
+        } else {
+          const uint32_t part = static_cast<uint32_t>(word >> (32 * t));
+          v = *reinterpret_cast<const T*>(&part);
+        }
+        T* d = dst + pat_index(s.dst, i) * bl + k;
+        if constexpr (OP == OP_REPLACE)
+          *d = v;
+        else
+          *d = apply_op<T, OP>(*d, v);
       }
-      T* d = dst + pat_index(s.dst, i) * bl + k;
-      if constexpr (OP == OP_REPLACE)
-        *d = v;
-      else
-        *d = apply_op<T, OP>(*d, v);
     }
   }
 }

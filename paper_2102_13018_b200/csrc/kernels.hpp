@@ -66,7 +66,8 @@ enum SegType : int32_t {
 // line starts as soon as it lands (NCCL's LL128 protocol). Each receive
 // region holds two messages per channel (parity m & 1), so a put waits only
 // for the acknowledgement of message m-2, which is long done.
-constexpr int kLLLines = 32;  // lines per CTA (4 per warp)
+constexpr int kLLIters = 4;                  // line groups per warp
+constexpr int kLLLines = 8 * 4 * kLLIters;  // lines per CTA (256 threads)
 
 // Buffer slots a segment can address; filled per call.
 enum BufId : int32_t {
@@ -184,6 +185,7 @@ struct LaunchParams {
   unsigned long long* done_flag[kMaxPeers];
   unsigned long long* done_seq[kMaxPeers];
   int ndone = 0;
+  int done_relaxed = 0;  // LL128 channels: acknowledge with a relaxed store
   unsigned int* done_count = nullptr;
   FetchShuffle shuf;
 };

@@ -193,6 +193,7 @@ struct Launch {
   unsigned int* done_count = nullptr;
   void* bufs[BUF_PEER0] = {};
   FetchShuffle shuffle;
+  bool done_relaxed = false;  // LL128 acknowledgements (kernels.cu st_relaxed_sys)
   bool any_op = false;
   const char* tag = "kernel";
 
@@ -355,6 +356,7 @@ struct Launch {
           ++p.ndone;
         }
         p.done_count = done_count;
+        p.done_relaxed = done_relaxed ? 1 : 0;
       }
       const int r = launch_segments(p, t, kop, st);
       SFG_REQUIRE(r >= 0, "no kernel instantiation for this unit/op combination");
@@ -713,6 +715,7 @@ void add_recvs_ll(OpHandle& h, Launch& L, const std::vector<DevPlan::Seg>& group
     sg.sig_seq = s.recvd(region, g.rank);
     L.add(sg, 0, -1, g.distinct);
     L.add_done(s.peer_free_flag(region, g.rank, me), s.recvd(region, g.rank), s.done_count);
+    L.done_relaxed = true;
     counters().bytes_recv += static_cast<uint64_t>(g.n) * h.unit.bytes();
     counters().unpack_copies++;
   }

@@ -167,6 +167,94 @@ __global__ void __launch_bounds__(256) reduce_B(double* root, const int* __restr
   }
 }
 
+// ---- improved two-phase (ILP: each thread issues all its loads first)
+// A2: CTA per root bucket; entries padded to a multiple of 8 per bucket (pad
+// entries write to a dummy slot); thread handles 8 consecutive entries with
+// 16-byte index loads.
+__global__ void __launch_bounds__(512) bcast_A2(const double* __restrict__ root, int R, int RB,
+                                                const int* __restrict__ eoff, const uint16_t* __restrict__ rootA,
+                                                const int* __restrict__ posA, double* __restrict__ S) {
+  extern __shared__ double tile[];
+  const int b = blockIdx.x;
+  const int r0 = b * RB, nr = min(RB, R - r0);
+  for (int i = threadIdx.x; i < nr; i += 512) tile[i] = root[r0 + i];
+  __syncthreads();
+  const int lo = eoff[b], hi = eoff[b + 1];  // multiples of 8
+  for (int e = lo + threadIdx.x * 8; e < hi; e += 512 * 8) {
+    const uint4 ra = *reinterpret_cast<const uint4*>(rootA + e);
+    const int4 p0 = *reinterpret_cast<const int4*>(posA + e);
+    const int4 p1 = *reinterpret_cast<const int4*>(posA + e + 4);
+    const uint16_t* r = reinterpret_cast<const uint16_t*>(&ra);
+    const int pp[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) S[pp[q]] = tile[r[q]];
+  }
+}
+
+// B2: CTA per leaf chunk (LC leaves), 512 threads, 16 loads in flight each.
+template <int LC>
+__global__ void __launch_bounds__(512) bcast_B2(const double* __restrict__ S, long long L,
+                                                const uint16_t* __restrict__ permB, double* __restrict__ leaf) {
+  extern __shared__ double tile[];
+  const long long c0 = (long long)blockIdx.x * LC;
+  constexpr int J = LC / 512;
+  double v[J];
+  uint16_t pk[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int k = j * 512 + threadIdx.x;
+    pk[j] = __ldg(permB + c0 + k);
+    v[j] = S[c0 + k];
+  }
+#pragma unroll
+  for (int j = 0; j < J; ++j) tile[pk[j]] = v[j];
+  __syncthreads();
+  double2* out = reinterpret_cast<double2*>(leaf + c0);
+  const double2* t2 = reinterpret_cast<const double2*>(tile);
+#pragma unroll
+  for (int j = 0; j < LC / 2 / 512; ++j) out[j * 512 + threadIdx.x] = t2[j * 512 + threadIdx.x];
+}
+
+// A'2: CTA per leaf chunk: tile = leaf chunk; S[posR[k]] = tile[permR[k]].
+template <int LC>
+__global__ void __launch_bounds__(512) reduce_A2(const double* __restrict__ leaf, const uint16_t* __restrict__ permR,
+                                                 const int* __restrict__ posR, double* __restrict__ S) {
+  extern __shared__ double tile[];
+  const long long c0 = (long long)blockIdx.x * LC;
+  const double2* in = reinterpret_cast<const double2*>(leaf + c0);
+  double2* t2 = reinterpret_cast<double2*>(tile);
+  constexpr int J = LC / 512;
+  uint16_t pk[J];
+  int ps[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    pk[j] = __ldg(permR + c0 + j * 512 + threadIdx.x);
+    ps[j] = __ldg(posR + c0 + j * 512 + threadIdx.x);
+  }
+#pragma unroll
+  for (int j = 0; j < LC / 2 / 512; ++j) t2[j * 512 + threadIdx.x] = in[j * 512 + threadIdx.x];
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < J; ++j) S[ps[j]] = tile[pk[j]];
+}
+
+// B'2: CTA per root bucket, 512 threads.
+__global__ void __launch_bounds__(512) reduce_B2(double* root, const int* __restrict__ rb, const int* __restrict__ sb,
+                                                 const int* __restrict__ roff, const uint16_t* __restrict__ rent,
+                                                 const double* __restrict__ S) {
+  extern __shared__ double tile[];
+  const int b = blockIdx.x;
+  const int s0 = sb[b], ns = sb[b + 1] - s0;
+  for (int k = threadIdx.x; k < ns; k += 512) tile[k] = S[s0 + k];
+  __syncthreads();
+  for (int r = rb[b] + threadIdx.x; r < rb[b + 1]; r += 512) {
+    double acc = root[r];
+    const int lo = roff[r], hi = roff[r + 1];
+    for (int j = lo; j < hi; ++j) acc = __dadd_rn(acc, tile[__ldg(rent + j)]);
+    root[r] = acc;
+  }
+}
+
 __global__ void flush_read(const double4* p, long long n, double* sink) {
   double a = 0;
   for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n; i += (long long)gridDim.x * 256) a += p[i].x;
@@ -333,6 +421,64 @@ static void config(const char* name, long long L, int R, int RB, int LC, Timer& 
   CK(cudaEventElapsedTime(&ta, m0, m1));
   CK(cudaEventElapsedTime(&tb, m1, m2));
   line("bcast", "2phase", us, bb, check_leaf("2phase"));
+  {
+    // padded copies of the bucket entry lists (dummy slot at L)
+    std::vector<int> eoff8(nb + 1, 0);
+    for (int b = 0; b < nb; ++b) eoff8[b + 1] = eoff8[b] + ((eoff[b + 1] - eoff[b] + 7) / 8) * 8;
+    std::vector<uint16_t> rootA8(eoff8[nb], 0);
+    std::vector<int> posA8(eoff8[nb], (int)L);
+    for (int b = 0; b < nb; ++b)
+      for (int e = eoff[b]; e < eoff[b + 1]; ++e) {
+        rootA8[eoff8[b] + e - eoff[b]] = rootA[e];
+        posA8[eoff8[b] + e - eoff[b]] = posA[e];
+      }
+    int *deoff8, *dposA8;
+    uint16_t* drootA8;
+    double* dS8;
+    CK(cudaMalloc(&deoff8, (nb + 1) * 4));
+    CK(cudaMalloc(&dposA8, eoff8[nb] * 4ll));
+    CK(cudaMalloc(&drootA8, eoff8[nb] * 2ll));
+    CK(cudaMalloc(&dS8, (L + 8) * 8));
+    CK(cudaMemcpy(deoff8, eoff8.data(), (nb + 1) * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dposA8, posA8.data(), eoff8[nb] * 4ll, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(drootA8, rootA8.data(), eoff8[nb] * 2ll, cudaMemcpyHostToDevice));
+    CK(cudaFuncSetAttribute(bcast_A2, cudaFuncAttributeMaxDynamicSharedMemorySize, RB * 8));
+    CK(cudaFuncSetAttribute(bcast_B2<8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8));
+    if (L % 8192 == 0) {
+      CK(cudaMemset(dleaf, 0, L * 8));
+      // B2 needs chunk-major S with chunks of 8192: rebuild permB for LC=8192
+      const int LC2 = 8192, nc2 = (int)(L / LC2);
+      std::vector<int> cnt2((size_t)nc2 * nb, 0);
+      for (long long i = 0; i < L; ++i) cnt2[(size_t)(i / LC2) * nb + idx[i] / RB]++;
+      std::vector<long long> cur2((size_t)nc2 * nb);
+      long long acc = 0;
+      for (size_t k = 0; k < cur2.size(); ++k) { cur2[k] = acc; acc += cnt2[k]; }
+      std::vector<uint16_t> permB2(L);
+      std::vector<int> bcur(eoff8.begin(), eoff8.end() - 1);
+      for (long long i = 0; i < L; ++i) {
+        const int b = idx[i] / RB;
+        const long long p = cur2[(size_t)(i / LC2) * nb + b]++;
+        permB2[p] = (uint16_t)(i % LC2);
+        const int e = bcur[b]++;
+        posA8[e] = (int)p;
+      }
+      CK(cudaMemcpy(dposA8, posA8.data(), eoff8[nb] * 4ll, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(dpermB, permB2.data(), L * 2, cudaMemcpyHostToDevice));
+      us = T.run([&] {
+        CK(cudaEventRecord(m0));
+        bcast_A2<<<nb, 512, RB * 8>>>(droot, R, RB, deoff8, drootA8, dposA8, dS8);
+        CK(cudaEventRecord(m1));
+        bcast_B2<8192><<<nc2, 512, 8192 * 8>>>(dS8, L, dpermB, dleaf);
+        CK(cudaEventRecord(m2));
+      });
+      CK(cudaEventSynchronize(m2));
+      CK(cudaEventElapsedTime(&ta, m0, m1));
+      CK(cudaEventElapsedTime(&tb, m1, m2));
+      line("bcast", "2phase_v2", us, bb, check_leaf("2phase_v2"));
+      std::printf("{\"config\":\"%s\",\"two_phase_bcast_v2\":{\"A_us\":%.2f,\"B_us\":%.2f}}\n", name, ta * 1000, tb * 1000);
+    }
+    cudaFree(deoff8); cudaFree(dposA8); cudaFree(drootA8); cudaFree(dS8);
+  }
   std::printf("{\"config\":\"%s\",\"two_phase_bcast\":{\"A_us\":%.2f,\"B_us\":%.2f,\"buckets\":%d,\"chunks\":%d}}\n", name,
               ta * 1000, tb * 1000, nb, nc);
 
@@ -423,6 +569,23 @@ static void config(const char* name, long long L, int R, int RB, int LC, Timer& 
   CK(cudaEventElapsedTime(&ta, m0, m1));
   CK(cudaEventElapsedTime(&tb, m1, m2));
   line("reduce", "2phase", (ta + tb) * 1000, rbytes, check_root());
+  if (LC == 8192 && L % 8192 == 0) {
+    CK(cudaFuncSetAttribute(reduce_A2<8192>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 8));
+    CK(cudaFuncSetAttribute(reduce_B2, cudaFuncAttributeMaxDynamicSharedMemorySize, SB * 8));
+    us = T.run([&] {
+      CK(cudaMemcpyAsync(dout, droot, R * 8ll, cudaMemcpyDeviceToDevice));
+      CK(cudaEventRecord(m0));
+      reduce_A2<8192><<<nc, 512, 8192 * 8>>>(dleaf, dpermR, dposR, dS);
+      CK(cudaEventRecord(m1));
+      reduce_B2<<<nbr, 512, SB * 8>>>(dout, drb, dsb, doff, drent, dS);
+      CK(cudaEventRecord(m2));
+    });
+    CK(cudaEventSynchronize(m2));
+    CK(cudaEventElapsedTime(&ta, m0, m1));
+    CK(cudaEventElapsedTime(&tb, m1, m2));
+    line("reduce", "2phase_v2", (ta + tb) * 1000, rbytes, check_root());
+    std::printf("{\"config\":\"%s\",\"two_phase_reduce_v2\":{\"A_us\":%.2f,\"B_us\":%.2f}}\n", name, ta * 1000, tb * 1000);
+  }
   std::printf("{\"config\":\"%s\",\"two_phase_reduce\":{\"A_us\":%.2f,\"B_us\":%.2f,\"buckets\":%d}}\n", name, ta * 1000,
               tb * 1000, nbr);
   cudaFree(droot); cudaFree(dout); cudaFree(dleaf); cudaFree(dS); cudaFree(didx); cudaFree(doff); cudaFree(dent);
@@ -432,7 +595,7 @@ static void config(const char* name, long long L, int R, int RB, int LC, Timer& 
 
 int main() {
   Timer T;
-  config("cfg1", 4194304, 1048576, 4096, 16384, T);
-  config("cfg4", 16777216, 65536, 4096, 16384, T);
+  config("cfg1", 4194304, 1048576, 4096, 8192, T);
+  config("cfg4", 16777216, 65536, 4096, 8192, T);
   return 0;
 }

@@ -128,9 +128,12 @@ __global__ void __launch_bounds__(256) flag_kernel(const __grid_constant__ Chan 
 
 // ------------------------------------------------------------- proto 1
 // line L of message m (parity m&1): words [L*16, L*16+15), word 15 = m.
-// Lane l of a warp covers line 4*it + l/8, words 2*(l%8), 2*(l%8)+1.
-__global__ void __launch_bounds__(256) ll128_kernel(const __grid_constant__ Chan c) {
+// Warp q, iteration u, lane l covers line 4*(IT*q + u) + l/8, words
+// 2*(l%8), 2*(l%8)+1. IT line groups per warp (loads first, then stores).
+template <int IT, bool REL>
+__device__ __forceinline__ void ll128_body(const Chan& c) {
   __shared__ u64 sm;
+  const int lines_per_cta = 8 * 4 * IT;
   const bool put = blockIdx.x < c.nput;
   if (threadIdx.x == 0) sm = put ? *c.sent + 1 : *c.recvd + 1;
   __syncthreads();
@@ -138,19 +141,24 @@ __global__ void __launch_bounds__(256) ll128_kernel(const __grid_constant__ Chan
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j = lane & 7;
   const long long par = static_cast<long long>(m & 1) * c.stage_words_per_parity;
+  const int b = put ? blockIdx.x : blockIdx.x - c.nput;
+  const long long L0 = (long long)b * lines_per_cta + warp * 4 * IT + (lane >> 3);
   if (put) {
     if (threadIdx.x == 0)
       while (ld_vol(c.my_free) + 2 < m) __nanosleep(32);  // peer consumed message m-2 (same parity)
     __syncthreads();
-    const long long nwarps = 8ll * c.nput;
-    for (long long g = (blockIdx.x * 8ll + warp); g * 4 < c.lines; g += nwarps) {
-      const long long L = g * 4 + (lane >> 3);
-      if (L < c.lines) {
-        const long long p0 = L * 15 + 2 * j;
-        const u64 a = p0 < c.n ? word(c, m, p0) : 0;
-        const u64 b = j == 7 ? m : (p0 + 1 < c.n ? word(c, m, p0 + 1) : 0);
-        st_v2_vol(c.peer_stage + par + L * 16 + 2 * j, a, b);
-      }
+    u64 a[IT], v[IT];
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+      const long long L = L0 + 4 * u;
+      const long long p0 = L * 15 + 2 * j;
+      a[u] = (L < c.lines && p0 < c.n) ? word(c, m, p0) : 0;
+      v[u] = j == 7 ? m : ((L < c.lines && p0 + 1 < c.n) ? word(c, m, p0 + 1) : 0);
+    }
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+      const long long L = L0 + 4 * u;
+      if (L < c.lines) st_v2_vol(c.peer_stage + par + L * 16 + 2 * j, a[u], v[u]);
     }
     __syncthreads();
     if (threadIdx.x == 0 && arrive(c.put_count) + 1 == static_cast<unsigned>(c.nput)) {
@@ -158,28 +166,33 @@ __global__ void __launch_bounds__(256) ll128_kernel(const __grid_constant__ Chan
       *c.sent = m;
     }
   } else {
-    const int b = blockIdx.x - c.nput, nb = gridDim.x - c.nput;
-    const long long nwarps = 8ll * nb;
-    for (long long g = (b * 8ll + warp); g * 4 < c.lines; g += nwarps) {
-      const long long L = g * 4 + (lane >> 3);
-      const bool live = L < c.lines;
-      u64 a = 0, v = 0;
-      for (;;) {
-        if (live) ld_v2_vol(c.my_stage + par + L * 16 + 2 * j, a, v);
-        const u64 f = __shfl_sync(0xffffffffu, v, (lane & ~7) | 7);
-        if (__all_sync(0xffffffffu, !live || f == m)) break;
-        __nanosleep(20);
+    u64 a[IT], v[IT];
+    for (;;) {
+      bool ok = true;
+#pragma unroll
+      for (int u = 0; u < IT; ++u) {
+        const long long L = L0 + 4 * u;
+        a[u] = 0;
+        v[u] = m;
+        if (L < c.lines) ld_v2_vol(c.my_stage + par + L * 16 + 2 * j, a[u], v[u]);
       }
-      if (live) {
-        const long long p0 = L * 15 + 2 * j;
-        if (p0 < c.n) {
-          c.dst[p0] = a;
-          if (c.verify && a != ((m << 40) ^ static_cast<u64>(p0))) atomicAdd(c.errors, 1ull);
-        }
-        if (j != 7 && p0 + 1 < c.n) {
-          c.dst[p0 + 1] = v;
-          if (c.verify && v != ((m << 40) ^ static_cast<u64>(p0 + 1))) atomicAdd(c.errors, 1ull);
-        }
+#pragma unroll
+      for (int u = 0; u < IT; ++u) ok = ok && __shfl_sync(0xffffffffu, v[u], (lane & ~7) | 7) == m;
+      if (__all_sync(0xffffffffu, ok)) break;
+      __nanosleep(20);
+    }
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+      const long long L = L0 + 4 * u;
+      if (L >= c.lines) break;
+      const long long p0 = L * 15 + 2 * j;
+      if (p0 < c.n) {
+        c.dst[p0] = a[u];
+        if (c.verify && a[u] != ((m << 40) ^ static_cast<u64>(p0))) atomicAdd(c.errors, 1ull);
+      }
+      if (j != 7 && p0 + 1 < c.n) {
+        c.dst[p0 + 1] = v[u];
+        if (c.verify && v[u] != ((m << 40) ^ static_cast<u64>(p0 + 1))) atomicAdd(c.errors, 1ull);
       }
     }
   }
@@ -187,9 +200,21 @@ __global__ void __launch_bounds__(256) ll128_kernel(const __grid_constant__ Chan
   if (threadIdx.x == 0 && arrive(c.all_count) + 1 == gridDim.x) {
     *c.all_count = 0;
     *c.recvd = m;
-    st_rlx_sys(c.peer_free, m);  // credit for message m (read 2 messages later)
+    if (REL)
+      st_rel_sys(c.peer_free, m);
+    else
+      st_rlx_sys(c.peer_free, m);  // credit for message m (read 2 messages later)
   }
 }
+
+template <int IT, bool REL>
+__global__ void __launch_bounds__(256) ll128_kernel(const __grid_constant__ Chan c) { ll128_body<IT, REL>(c); }
+
+struct ChanPad {  // the library's launch parameter block is ~5 KB
+  Chan c;
+  char pad[5120];
+};
+__global__ void __launch_bounds__(256) ll128_kernel_pad(const __grid_constant__ ChanPad c) { ll128_body<4, false>(c.c); }
 
 int main(int argc, char** argv) {
   int ndev = 0;
@@ -253,19 +278,28 @@ int main(int argc, char** argv) {
     c.lines = (n + 14) / 15;
     c.stage_words_per_parity = maxlines * 16;
     c.verify = verify;
-    const long long per_cta = proto == 1 ? 8 * 4 * 4 * 15 : 256 * 8;  // words per CTA
+    const long long per_cta = proto == 0 ? 256 * 8 : proto == 2 ? 8 * 4 * 15 : 8 * 4 * 4 * 15;  // words per CTA
     c.nput = static_cast<int>(std::max(1ll, std::min(592ll, (n + per_cta - 1) / per_cta)));
     return c;
   };
   auto launch = [&](int d, const Chan& c, int proto) {
-    if (proto == 0)
+    if (proto == 0) {
       flag_kernel<<<2 * c.nput, 256, 0, D[d].s>>>(c);
-    else
-      ll128_kernel<<<2 * c.nput, 256, 0, D[d].s>>>(c);
+    } else if (proto == 1) {
+      ll128_kernel<4, false><<<2 * c.nput, 256, 0, D[d].s>>>(c);
+    } else if (proto == 2) {
+      ll128_kernel<1, false><<<2 * c.nput, 256, 0, D[d].s>>>(c);
+    } else if (proto == 3) {
+      ll128_kernel<4, true><<<2 * c.nput, 256, 0, D[d].s>>>(c);
+    } else {
+      ChanPad cp{};
+      cp.c = c;
+      ll128_kernel_pad<<<2 * c.nput, 256, 0, D[d].s>>>(cp);
+    }
   };
-  const char* pname[2] = {"flag", "ll128"};
+  const char* pname[5] = {"flag", "ll128", "ll128_it1", "ll128_release_ack", "ll128_5KB_params"};
   // 1. integrity: many exchanges with changing data, every word checked
-  for (int proto = 0; proto < 2; ++proto) {
+  for (int proto = 0; proto < 5; proto += 1) {
     for (long long bytes : {8ll, 4096ll, 262144ll, 2097152ll}) {
       reset();
       const long long n = bytes / 8;
@@ -287,7 +321,7 @@ int main(int argc, char** argv) {
     }
   }
   // 2. latency / bandwidth: K exchanges per graph, per exchange time
-  for (int proto = 0; proto < 2; ++proto) {
+  for (int proto = 0; proto < 5; ++proto) {
     for (long long bytes = 8; bytes <= (32ll << 20); bytes *= 4) {
       reset();
       const long long n = bytes / 8;

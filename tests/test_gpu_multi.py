@@ -268,3 +268,59 @@ def test_process_per_gpu_torchrun(backend):
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "mp_worker ok" in r.stdout
+
+
+def _counted(specs, opkind, data, op, backend, n):
+    sf.counters_reset()
+    run_gpu(specs, opkind, data, op=op, config=sf.CommConfig(backend=backend), devices=list(range(n)))
+    return sf.counters()
+
+
+@need2
+def test_pattern_elision_counters_nccl():
+    """SPEC.md:562 (acceptance 7, test_pack.cpp:24-37): the ping-pong SF and
+    the SpMV ghost SF move contiguous groups without a staging copy on the
+    contiguous side (sends straight from user memory, REPLACE receives
+    straight into it); an Indexed-pattern control pays pack copies."""
+    n = 1 << 10
+    pp = graphs.pingpong(8 * n)
+    roots = [np.arange(n, dtype=np.int64), np.zeros(0, np.int64)]
+    leaves = [np.zeros(0, np.int64), np.zeros(n, np.int64)]
+    c = _counted(pp, "bcast", [roots, leaves], "replace", "nccl", 2)
+    assert c["pack_copies"] == 0 and c["unpack_copies"] == 0, c
+    assert c["pack_elided"] == 1 and c["unpack_elided"] == 1, c
+    c = _counted(pp, "reduce", [[np.zeros(0, np.int64), np.arange(n, dtype=np.int64)],
+                                [np.zeros(n, np.int64), np.zeros(0, np.int64)]], "replace", "nccl", 2)
+    assert c["pack_copies"] == 0 and c["unpack_copies"] == 0, c
+    # SpMV ghost SF (build_column_sf shape): leaves = contiguous lvec
+    ghost = [graphs.laplacian27_ghosts(12, (1, 1, 2), r) for r in range(2)]
+    groots = [graphs.gen_f64(1, r, int(s.nroots)) for r, s in enumerate(ghost)]
+    gleaves = [np.zeros(s.leaf_bound()) for s in ghost]
+    c = _counted(ghost, "bcast", [groots, gleaves], "replace", "nccl", 2)
+    assert c["unpack_copies"] == 0 and c["unpack_elided"] == 2, c  # contiguous leaf side
+    c = _counted(ghost, "reduce", [gleaves, groots], "sum", "nccl", 2)
+    assert c["pack_copies"] == 0 and c["pack_elided"] == 2, c  # transpose SpMV: leaf side sends
+    # Indexed control: leaves listed in shuffled order -> packs pay copies
+    ctl = graphs.random_graph_specs(17, 2, 60)
+    croots = rank_data(ctl, 1, np.int64, 1, 100, "root")
+    cleaves = rank_data(ctl, 1, np.int64, 1, 200, "leaf")
+    c = _counted(ctl, "reduce", [cleaves, croots], "sum", "nccl", 2)
+    assert c["pack_copies"] > 0, c
+
+
+@need2
+def test_p2p_puts_never_stage_on_the_sender():
+    """The p2p puts gather straight from the caller's buffer into the peer's
+    receive region (the pack is fused into the put): no pack copy at all, on
+    contiguous and Indexed patterns alike."""
+    n = 1 << 10
+    pp = graphs.pingpong(8 * n)
+    roots = [np.arange(n, dtype=np.int64), np.zeros(0, np.int64)]
+    leaves = [np.zeros(0, np.int64), np.zeros(n, np.int64)]
+    c = _counted(pp, "bcast", [roots, leaves], "replace", "p2p", 2)
+    assert c["pack_copies"] == 0 and c["pack_elided"] == 1, c
+    ctl = graphs.random_graph_specs(17, 2, 60)
+    croots = rank_data(ctl, 1, np.int64, 1, 100, "root")
+    cleaves = rank_data(ctl, 1, np.int64, 1, 200, "leaf")
+    c = _counted(ctl, "reduce", [cleaves, croots], "sum", "p2p", 2)
+    assert c["pack_copies"] == 0 and c["pack_elided"] > 0, c
