@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "kernels.hpp"
@@ -122,8 +123,8 @@ __device__ __forceinline__ bool skipped(const uint32_t* bits, int64_t v) {
 }
 
 // dst[dpat(i)] (op)= src[spat(i)] over this CTA's items.
-template <class T, int OP>
-__device__ __forceinline__ void run_pair(const DSeg& s, const LaunchParams& P, int64_t blk) {
+template <class T, int OP, class PP>
+__device__ __forceinline__ void run_pair(const DSeg& s, const PP& P, int64_t blk) {
   const T* __restrict__ src = static_cast<const T*>(P.bufs[s.src_buf]);
   T* dst = static_cast<T*>(P.bufs[s.dst_buf]);
   const int64_t total = s.n * P.bl;
@@ -165,8 +166,8 @@ __device__ __forceinline__ void run_pair(const DSeg& s, const LaunchParams& P, i
 // consecutive elements of the CTA's chunk; index maps are evaluated once per
 // run (not per element), then the lanes stream the run with kItems
 // independent loads in flight each.
-template <class T, int OP>
-__device__ __forceinline__ void run_pair_rows(const DSeg& s, const LaunchParams& P, int64_t blk) {
+template <class T, int OP, class PP>
+__device__ __forceinline__ void run_pair_rows(const DSeg& s, const PP& P, int64_t blk) {
   const T* __restrict__ src = static_cast<const T*>(P.bufs[s.src_buf]);
   T* dst = static_cast<T*>(P.bufs[s.dst_buf]);
   const int64_t bl = P.bl;
@@ -335,8 +336,8 @@ __device__ __forceinline__ int32_t shuf_bound(const FetchShuffle& f, const int32
 // the CPU reference, and a warp instruction advances 32 roots at once.
 // With pieces (csr_np > 1) the grid walks L2-sized leaf windows piece-major
 // (see run_csr_warp).
-template <class T, int OP, int kB, bool FETCH>
-__device__ __forceinline__ void run_csr_t(const DSeg& s, const LaunchParams& P, int64_t blk) {
+template <class T, int OP, int kB, bool FETCH, class PP>
+__device__ __forceinline__ void run_csr_t(const DSeg& s, const PP& P, int64_t blk) {
   T* root = static_cast<T*>(P.bufs[s.dst_buf]);
   const T* leaf = static_cast<const T*>(P.bufs[s.src_buf]);
   T* stage = static_cast<T*>(P.bufs[s.stage_buf]);
@@ -385,9 +386,9 @@ __device__ __forceinline__ void run_csr_t(const DSeg& s, const LaunchParams& P, 
 template <class T, int OP, int kB = 8>
 __device__ __forceinline__ void run_csr(const DSeg& s, const LaunchParams& P, int64_t blk, bool fetch) {
   if (fetch)
-    run_csr_t<T, OP, kB, true>(s, P, blk);
+    run_csr_t<T, OP, kB, true, LaunchParams>(s, P, blk);
   else
-    run_csr_t<T, OP, kB, false>(s, P, blk);
+    run_csr_t<T, OP, kB, false, LaunchParams>(s, P, blk);
 }
 
 // One warp folds contributions [lo, hi) of one root item into acc (held by
@@ -704,7 +705,10 @@ __device__ __forceinline__ void run_recv_ll(const DSeg& s, const LaunchParams& P
       if (L < lines) ld_v2_volatile(reg + (s.ll_line + L) * 16 + 2 * j, a[u], b[u]);
     }
 #pragma unroll
-    for (int u = 0; u < kLLIters; ++u) ok = ok && __shfl_sync(0xffffffffu, b[u], (lane & ~7) | 7) == m;
+    for (int u = 0; u < kLLIters; ++u) {
+      const unsigned long long f = __shfl_sync(0xffffffffu, b[u], (lane & ~7) | 7);  // every lane
+      ok = ok && f == m;
+    }
     if (__all_sync(0xffffffffu, ok)) break;
     __nanosleep(20);
     if (global_ns() - t0 > 30000000000ull) {
@@ -771,14 +775,14 @@ __global__ void __launch_bounds__(kThreads, FULL ? 3 : 4) segments_kernel(const 
     case SEG_PAIR:
       if (seg.run > 0) {
         if (seg.replace)
-          run_pair_rows<T, OP_REPLACE>(seg, P, blk);
+          run_pair_rows<T, OP_REPLACE, LaunchParams>(seg, P, blk);
         else
-          run_pair_rows<T, OP>(seg, P, blk);
+          run_pair_rows<T, OP, LaunchParams>(seg, P, blk);
       } else {
         if (seg.replace)
-          run_pair<T, OP_REPLACE>(seg, P, blk);
+          run_pair<T, OP_REPLACE, LaunchParams>(seg, P, blk);
         else
-          run_pair<T, OP>(seg, P, blk);
+          run_pair<T, OP, LaunchParams>(seg, P, blk);
       }
       break;
     case SEG_PUT_LL:
@@ -826,8 +830,51 @@ template <class T, int OP, bool FETCH>
 __global__ void __launch_bounds__(kThreads, 4) csr_kernel(const __grid_constant__ LaunchParams P) {
   const DSeg& seg = P.seg[0];
   if (seg.wait_mask) wait_flags(P, seg.wait_mask);
-  if constexpr (OP != OP_REPLACE) run_csr_t<T, OP, 8, FETCH>(seg, P, blockIdx.x);
+  if constexpr (OP != OP_REPLACE) run_csr_t<T, OP, 8, FETCH, LaunchParams>(seg, P, blockIdx.x);
   if (P.ndone > 0) signal_launch_done(P);
+}
+
+// A launch that is ONE pair or CSR segment with no p2p waits or signals (a
+// local scatter, a gather, a self-only fold) runs from a compact parameter
+// block (~0.6 KB instead of LaunchParams' ~5 KB).
+struct SoloParams {
+  DSeg seg;
+  void* bufs[BUF_COUNT];
+  int64_t bl = 1;
+  FastDiv bldiv;
+  int64_t wpv = 1;
+  FetchShuffle shuf;
+};
+
+template <class T, int OP>
+__global__ void __launch_bounds__(kThreads, 4) pair_solo(const __grid_constant__ SoloParams P) {
+  if (P.seg.run > 0)
+    run_pair_rows<T, OP, SoloParams>(P.seg, P, blockIdx.x);
+  else
+    run_pair<T, OP, SoloParams>(P.seg, P, blockIdx.x);
+}
+
+template <class T, int OP, bool FETCH>
+__global__ void __launch_bounds__(kThreads, 4) csr_solo(const __grid_constant__ SoloParams P) {
+  if constexpr (OP != OP_REPLACE) run_csr_t<T, OP, 8, FETCH, SoloParams>(P.seg, P, blockIdx.x);
+}
+
+bool solo_ok(const LaunchParams& p) {
+  if (p.nseg != 1 || p.ndone != 0) return false;
+  const DSeg& g = p.seg[0];
+  if (g.wait_mask || g.sig_flag || g.sig_count) return false;
+  return g.type == SEG_PAIR || ((g.type == SEG_CSR_FOLD || g.type == SEG_CSR_FETCH) && !g.csr_warp);
+}
+
+SoloParams solo_of(const LaunchParams& p) {
+  SoloParams q;
+  q.seg = p.seg[0];
+  for (int b = 0; b < BUF_COUNT; ++b) q.bufs[b] = p.bufs[b];
+  q.bl = p.bl;
+  q.bldiv = p.bldiv;
+  q.wpv = p.wpv;
+  q.shuf = p.shuf;
+  return q;
 }
 
 template <class T, int OP>
@@ -835,6 +882,25 @@ void launch_t(const LaunchParams& p, int64_t blocks, cudaStream_t st) {
   bool full = false;
   for (int s = 0; s < p.nseg; ++s)
     full = full || p.seg[s].type != SEG_PAIR;
+  static const bool no_solo = std::getenv("SFG_NO_SOLO") != nullptr;  // ablation
+  if (!no_solo && solo_ok(p)) {
+    const SoloParams q = solo_of(p);
+    if (p.seg[0].type == SEG_PAIR) {
+      if (p.seg[0].replace)
+        pair_solo<T, OP_REPLACE><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(q);
+      else
+        pair_solo<T, OP><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(q);
+      return;
+    }
+    if constexpr (OP != OP_REPLACE && (std::is_same_v<T, double> || std::is_same_v<T, int64_t> ||
+                                       std::is_same_v<T, int32_t>)) {
+      if (p.seg[0].type == SEG_CSR_FETCH)
+        csr_solo<T, OP, true><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(q);
+      else
+        csr_solo<T, OP, false><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(q);
+      return;
+    }
+  }
   if constexpr (OP == OP_REPLACE) {
     segments_kernel<T, OP, false><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
   } else if (p.nseg == 1 && (p.seg[0].type == SEG_CSR_FOLD || p.seg[0].type == SEG_CSR_FETCH) &&
@@ -906,7 +972,10 @@ int64_t resident_full() {
     int c = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, csr_kernel<T, OP, false>, kThreads, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, csr_kernel<T, OP, true>, kThreads, 0);
-    const int per_sm = std::min(a, std::min(b, c));
+    int d1 = 0, d2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d1, csr_solo<T, OP, false>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d2, csr_solo<T, OP, true>, kThreads, 0);
+    const int per_sm = std::min(std::min(a, std::min(b, c)), std::min(d1, d2));
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     return static_cast<int64_t>(std::max(1, per_sm) * std::max(1, sms));

@@ -719,8 +719,28 @@ bool stream_capturing(cudaStream_t s) { return capture_id(s) != 0; }
 void StarForest::prepare(size_t ub) {
   require_state(SfState::set_up, "prepare");
   if (!comm_->has_device()) return;
+  // The local part may fail on one rank only (an index beyond the device
+  // plans' int32 range); the p2p slot attachment below is collective, so
+  // every rank learns whether all of them got this far before entering it.
+  std::string err;
+  try {
+    DevPlan& d0 = dev();
+    if ((d0.self_root_dups || d0.remote_root_dups) && !d0.csr_built) ensure_csr();
+  } catch (const CudaError&) {
+    throw;
+  } catch (const Error& e) {
+    err = e.what();
+  }
+  if (comm_->p2p() && comm_->size() > 1) {
+    const int32_t mine = err.empty() ? 0 : 1;
+    std::vector<int32_t> all(static_cast<size_t>(comm_->size()));
+    comm_->ctrl().allgather(&mine, sizeof(mine), all.data());
+    for (size_t r = 0; r < all.size() && err.empty(); ++r)
+      if (all[r]) err = "prepare: the device plan failed on rank " + std::to_string(r);
+  }
+  if (!err.empty()) fail(err);
   DevPlan& d = dev();
-  if ((d.self_root_dups || d.remote_root_dups) && !d.csr_built) ensure_csr();
+  (void)d;
   for (auto& s : staging_)
     if (!s->in_use && !s->retired && s->unit_bytes == ub) return;
   release_staging(acquire_staging(ub, cudaStreamPerThread), cudaStreamPerThread);

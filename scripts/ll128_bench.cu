@@ -177,7 +177,10 @@ __device__ __forceinline__ void ll128_body(const Chan& c) {
         if (L < c.lines) ld_v2_vol(c.my_stage + par + L * 16 + 2 * j, a[u], v[u]);
       }
 #pragma unroll
-      for (int u = 0; u < IT; ++u) ok = ok && __shfl_sync(0xffffffffu, v[u], (lane & ~7) | 7) == m;
+      for (int u = 0; u < IT; ++u) {
+        const u64 f = __shfl_sync(0xffffffffu, v[u], (lane & ~7) | 7);  // every lane
+        ok = ok && f == m;
+      }
       if (__all_sync(0xffffffffu, ok)) break;
       __nanosleep(20);
     }
@@ -279,7 +282,8 @@ int main(int argc, char** argv) {
     c.stage_words_per_parity = maxlines * 16;
     c.verify = verify;
     const long long per_cta = proto == 0 ? 256 * 8 : proto == 2 ? 8 * 4 * 15 : 8 * 4 * 4 * 15;  // words per CTA
-    c.nput = static_cast<int>(std::max(1ll, std::min(592ll, (n + per_cta - 1) / per_cta)));
+    c.nput = static_cast<int>(std::max(1ll, (n + per_cta - 1) / per_cta));
+    if (proto == 0) c.nput = std::min(c.nput, 592);  // grid-stride loops
     return c;
   };
   auto launch = [&](int d, const Chan& c, int proto) {
