@@ -763,12 +763,28 @@ __device__ __forceinline__ void count_put_ll(const DSeg& seg, int64_t nblk) {
 // FULL = the launch contains root-sorted (CSR) or fetch segments. Pair-only
 // launches (every pack, unpack and structured local scatter) get their own
 // instantiation so the CSR paths do not raise their register allocation.
-template <class T, int OP, bool FULL>
-__global__ void __launch_bounds__(kThreads, FULL ? 3 : 4) segments_kernel(const __grid_constant__ LaunchParams P) {
+// MODE 0: pair segments only (4 CTAs/SM); 1 (FULL): CSR / fetch segments
+// too (3 CTAs/SM); 2: pair + LL128 put/receive segments (2 CTAs/SM: the
+// receive keeps 4 lines x 16 bytes per lane in flight without spilling).
+template <class T, int OP, int MODE>
+__global__ void __launch_bounds__(kThreads, MODE == 0 ? 4 : MODE == 1 ? 3 : 2)
+    segments_kernel(const __grid_constant__ LaunchParams P) {
+  constexpr bool FULL = MODE == 1;
   const int64_t b = blockIdx.x;
   int s = 0;
   while (s + 1 < P.nseg && b >= P.block_start[s + 1]) ++s;
-  const DSeg& seg = P.seg[s];
+  // The CTA's segment descriptor, copied once into shared memory: reading it
+  // straight from the parameter block with a run-time segment index costs
+  // indexed constant loads and register pressure (a 64-byte stack frame) in
+  // every item loop — the single-segment form without it (pair_solo) ran
+  // the config 1 gather 20 % faster.
+  __shared__ DSeg sseg;
+  static_assert(sizeof(DSeg) % 8 == 0, "DSeg copied as 8-byte words");
+  if (threadIdx.x < sizeof(DSeg) / 8)
+    reinterpret_cast<unsigned long long*>(&sseg)[threadIdx.x] =
+        reinterpret_cast<const unsigned long long*>(&P.seg[s])[threadIdx.x];
+  __syncthreads();
+  const DSeg& seg = sseg;
   const int64_t blk = b - P.block_start[s];
   if (seg.wait_mask) wait_flags(P, seg.wait_mask);
   switch (seg.type) {
@@ -786,10 +802,10 @@ __global__ void __launch_bounds__(kThreads, FULL ? 3 : 4) segments_kernel(const 
       }
       break;
     case SEG_PUT_LL:
-      if constexpr (sizeof(T) >= 4) run_put_ll(seg, P, blk);
+      if constexpr (sizeof(T) >= 4 && MODE != 0) run_put_ll(seg, P, blk);
       break;
     case SEG_RECV_LL:
-      if constexpr (sizeof(T) >= 4) {
+      if constexpr (sizeof(T) >= 4 && MODE != 0) {
         if (seg.replace)
           run_recv_ll<T, OP_REPLACE>(seg, P, blk);
         else
@@ -901,8 +917,12 @@ void launch_t(const LaunchParams& p, int64_t blocks, cudaStream_t st) {
       return;
     }
   }
-  if constexpr (OP == OP_REPLACE) {
-    segments_kernel<T, OP, false><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
+  bool ll = false;
+  for (int s = 0; s < p.nseg; ++s) ll = ll || p.seg[s].type == SEG_PUT_LL || p.seg[s].type == SEG_RECV_LL;
+  if (ll && !full) {
+    segments_kernel<T, OP, 2><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
+  } else if constexpr (OP == OP_REPLACE) {
+    segments_kernel<T, OP, 0><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
   } else if (p.nseg == 1 && (p.seg[0].type == SEG_CSR_FOLD || p.seg[0].type == SEG_CSR_FETCH) &&
              !p.seg[0].csr_warp && (std::is_same_v<T, double> || std::is_same_v<T, int64_t> ||
                                     std::is_same_v<T, int32_t>)) {
@@ -912,9 +932,9 @@ void launch_t(const LaunchParams& p, int64_t blocks, cudaStream_t st) {
       csr_kernel<T, OP, false><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
   } else {
     if (full)
-      segments_kernel<T, OP, true><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
+      segments_kernel<T, OP, 1><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
     else
-      segments_kernel<T, OP, false><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
+      segments_kernel<T, OP, 0><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
   }
 }
 
@@ -968,7 +988,7 @@ int64_t resident_full() {
   static const int64_t v = [] {
     int dev = 0, sms = 0, a = 0, b = 0;
     // the smaller residency of the two kernels a CSR segment may run in
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, segments_kernel<T, OP, true>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, segments_kernel<T, OP, 1>, kThreads, 0);
     int c = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, csr_kernel<T, OP, false>, kThreads, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, csr_kernel<T, OP, true>, kThreads, 0);
