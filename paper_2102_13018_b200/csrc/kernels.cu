@@ -778,13 +778,13 @@ __global__ void __launch_bounds__(kThreads, MODE == 0 ? 4 : MODE == 1 ? 3 : 2)
   // indexed constant loads and register pressure (a 64-byte stack frame) in
   // every item loop — the single-segment form without it (pair_solo) ran
   // the config 1 gather 20 % faster.
-  __shared__ DSeg sseg;
+  // (raw storage: a __shared__ DSeg would not run DSeg's member initialisers,
+  // and must not)
+  __shared__ alignas(8) unsigned long long sseg[sizeof(DSeg) / 8];
   static_assert(sizeof(DSeg) % 8 == 0, "DSeg copied as 8-byte words");
-  if (threadIdx.x < sizeof(DSeg) / 8)
-    reinterpret_cast<unsigned long long*>(&sseg)[threadIdx.x] =
-        reinterpret_cast<const unsigned long long*>(&P.seg[s])[threadIdx.x];
+  if (threadIdx.x < sizeof(DSeg) / 8) sseg[threadIdx.x] = reinterpret_cast<const unsigned long long*>(&P.seg[s])[threadIdx.x];
   __syncthreads();
-  const DSeg& seg = sseg;
+  const DSeg& seg = *reinterpret_cast<const DSeg*>(sseg);
   const int64_t blk = b - P.block_start[s];
   if (seg.wait_mask) wait_flags(P, seg.wait_mask);
   switch (seg.type) {
@@ -895,9 +895,9 @@ SoloParams solo_of(const LaunchParams& p) {
 
 template <class T, int OP>
 void launch_t(const LaunchParams& p, int64_t blocks, cudaStream_t st) {
-  bool full = false;
+  bool full = false;  // CSR / fetch segments present
   for (int s = 0; s < p.nseg; ++s)
-    full = full || p.seg[s].type != SEG_PAIR;
+    full = full || p.seg[s].type == SEG_CSR_FOLD || p.seg[s].type == SEG_CSR_FETCH;
   static const bool no_solo = std::getenv("SFG_NO_SOLO") != nullptr;  // ablation
   if (!no_solo && solo_ok(p)) {
     const SoloParams q = solo_of(p);
