@@ -148,6 +148,10 @@ def timed_graph(ctx, fn, steps, warmup, reps=5):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ctx.barrier()
         with torch.cuda.stream(ctx.stream):
+            # the first replay absorbs the ranks' start skew after the
+            # barrier (their exchanges couple them); the second, issued right
+            # behind it, is timed: the steady-state period per call
+            g.replay()
             e0.record(ctx.stream)
             g.replay()
             e1.record(ctx.stream)

@@ -594,10 +594,20 @@ void p2p_begin(OpHandle& h, Launch& pack, Launch& local,
     local.run(h.unit, h.op, h.stream);
     return;
   }
+  static const bool no_fork = std::getenv("SFG_P2P_NO_FORK") != nullptr;  // ablation
+  const bool fuse_local = local.algorithmic_bytes(h.unit) < kFuseLocalBytes;
+  if (no_fork && fuse_local) {
+    pack.absorb(local);
+    pack.tag = tag_of(h, 0);
+    if (append_last) append_last(pack);
+    pack.run(h.unit, h.op, h.stream);
+    counters().transport_calls++;
+    return;
+  }
   cudaStream_t cs = c.comm_stream();
   c.fork(h.stream);
   h.forked = true;
-  if (local.algorithmic_bytes(h.unit) < kFuseLocalBytes) {
+  if (fuse_local) {
     pack.absorb(local);
     pack.tag = tag_of(h, 0);
     if (append_last) append_last(pack);
