@@ -319,6 +319,20 @@ def config2(ctx, args):
         h = sf.reduce_begin(f, u, leaf, root, sf.ReduceOp.sum, ctx.stream)
         sf.reduce_end(h)
 
+    if os.environ.get("SFG_TRACE_LAUNCHES"):
+        # debug: in-kernel timestamps of 20 captured Bcasts, replayed once
+        g = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=ctx.stream):
+            for _ in range(20):
+                bc()
+        torch.cuda.synchronize()
+        ctx.barrier()
+        g.replay()
+        torch.cuda.synchronize()
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        sf._lib().sfg_trace_dump(os.path.join(ROOT, "gpurun_out", f"trace_cfg2_r{ctx.rank}.jsonl").encode())
+        del g
     for name, fn in (("bcast_replace", bc), ("reduce_sum", rd)):
         ms, byts, rec = ctx.timed(fn, args.steps, args.warmup, flush=False)
         gms = timed_graph(ctx, fn, args.steps, args.warmup)

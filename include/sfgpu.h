@@ -240,6 +240,10 @@ typedef struct sfg_timing {
   double bytes;
   double link_bytes; /* bytes stored into peer GPUs' memory (p2p puts) */
 } sfg_timing;
+/* Debug: with SFG_TRACE_LAUNCHES=N in the environment, %globaltimer marks
+ * of the first N multi-segment launches (put / receive CTA start and end,
+ * LL data ready, launch end) are written to `path` as JSON lines. */
+int sfg_trace_dump(const char* path);
 int sfg_timing_enable(int on);
 int sfg_timing_collect(sfg_timing* out, int cap, int* n);
 

@@ -127,6 +127,7 @@ _SIGS = {
     "sfg_counters_get": (C.c_int, [C.POINTER(sfg_counters)]),
     "sfg_counters_reset": (C.c_int, []),
     "sfg_timing_enable": (C.c_int, [C.c_int]),
+    "sfg_trace_dump": (C.c_int, [C.c_char_p]),
     "sfg_timing_collect": (C.c_int, [_V, C.c_int, C.POINTER(C.c_int)]),
 }
 

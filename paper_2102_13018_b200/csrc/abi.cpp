@@ -490,6 +490,10 @@ int sfg_pattern_analyze(const int64_t* idx, int64_t n, int infer_affine, int64_t
   return guard([&] { fill_pattern(sfg::Pattern::analyze(idx, n, infer_affine != 0, ex, exy), out); });
 }
 
+int sfg_trace_dump(const char* path) {
+  return guard([&] { sfg::trace_dump(path); });
+}
+
 int sfg_counters_get(sfg_counters* o) {
   return guard([&] {
     auto& c = sfg::counters();

@@ -620,6 +620,12 @@ __device__ __forceinline__ void signal_segment_done(const DSeg& seg, int64_t nbl
   }
 }
 
+// Debug trace: word k of the launch's slot keeps max(value); start times are
+// stored as ~t so that max() keeps the earliest.
+__device__ __forceinline__ void trace_mark(unsigned long long* slot, int k, unsigned long long v) {
+  if (slot != nullptr && threadIdx.x == 0) atomicMax(slot + k, v);
+}
+
 // ------------------------------------------------------------ LL128 (p2p)
 __device__ __forceinline__ void st_v2_volatile(unsigned long long* p, unsigned long long a,
                                                unsigned long long b) {
@@ -680,8 +686,8 @@ __device__ __forceinline__ void run_put_ll(const DSeg& s, const LaunchParams& P,
 
 // Receive: poll this thread's lines until every flag is m, then apply each
 // data word's elements to dst[pat(vertex)] (op; REPLACE copies).
-template <class T, int OP>
-__device__ __forceinline__ void run_recv_ll(const DSeg& s, const LaunchParams& P, int64_t blk) {
+template <class T, int OP, class PP = LaunchParams>
+__device__ __forceinline__ void run_recv_ll(const DSeg& s, const PP& P, int64_t blk) {
   const unsigned long long m = ll_message(s.sig_seq);
   const auto* reg = static_cast<const unsigned long long*>(P.bufs[s.src_buf]) + static_cast<int64_t>(m & 1) * s.ll_par;
   T* dst = static_cast<T*>(P.bufs[s.dst_buf]);
@@ -716,6 +722,8 @@ __device__ __forceinline__ void run_recv_ll(const DSeg& s, const LaunchParams& P
       __trap();
     }
   }
+  if constexpr (std::is_same_v<PP, LaunchParams>)
+    if (P.trace && lane == 0) atomicMax(P.trace + 3, global_ns());
   const int64_t bl = P.bl;
 #pragma unroll
   for (int u = 0; u < kLLIters; ++u) {
@@ -771,6 +779,7 @@ __global__ void __launch_bounds__(kThreads, MODE == 0 ? 4 : MODE == 1 ? 3 : 2)
     segments_kernel(const __grid_constant__ LaunchParams P) {
   constexpr bool FULL = MODE == 1;
   const int64_t b = blockIdx.x;
+  const unsigned long long t_start = P.trace ? global_ns() : 0;
   int s = 0;
   while (s + 1 < P.nseg && b >= P.block_start[s + 1]) ++s;
   // The CTA's segment descriptor, copied once into shared memory: reading it
@@ -831,11 +840,20 @@ __global__ void __launch_bounds__(kThreads, MODE == 0 ? 4 : MODE == 1 ? 3 : 2)
     default:
       break;
   }
+  if (P.trace) {
+    const unsigned long long t_end = global_ns();
+    const int k = seg.type == SEG_PUT_LL ? 0 : seg.type == SEG_RECV_LL ? 2 : 6;
+    trace_mark(P.trace, k, ~t_start);
+    if (k < 6) trace_mark(P.trace, k + 1, t_end);
+    if (k == 2) trace_mark(P.trace, 4, t_end);
+    trace_mark(P.trace, 7, ~t_start);
+  }
   if (seg.type == SEG_PUT_LL)
     count_put_ll(seg, P.block_start[s + 1] - P.block_start[s]);
   else if (seg.sig_flag != nullptr)
     signal_segment_done(seg, P.block_start[s + 1] - P.block_start[s]);
   if (P.ndone > 0) signal_launch_done(P);
+  if (P.trace) trace_mark(P.trace, 5, global_ns());
 }
 
 // A launch that is one thread-per-root CSR segment runs in its own kernel,
@@ -1117,6 +1135,49 @@ void batched(unsigned long long* const* flag, unsigned long long* const* seq, in
     }
     k(q);
   }
+}
+
+namespace {
+struct TraceBuf {
+  unsigned long long* dev = nullptr;
+  int cap = 0, next = 0;
+  TraceBuf() {
+    const char* e = std::getenv("SFG_TRACE_LAUNCHES");
+    cap = e ? std::atoi(e) : 0;
+    if (cap > 0 && cudaMalloc(&dev, static_cast<size_t>(cap) * 64) == cudaSuccess)
+      cudaMemset(dev, 0, static_cast<size_t>(cap) * 64);
+    else
+      cap = 0;
+  }
+};
+TraceBuf& tbuf() {
+  static TraceBuf t;
+  return t;
+}
+}  // namespace
+
+unsigned long long* trace_slot() {
+  TraceBuf& t = tbuf();
+  if (t.cap == 0 || t.next >= t.cap) return nullptr;
+  return t.dev + 8 * static_cast<size_t>(t.next++);
+}
+
+void trace_dump(const char* path) {
+  TraceBuf& t = tbuf();
+  if (t.cap == 0) return;
+  std::vector<unsigned long long> h(static_cast<size_t>(t.next) * 8);
+  cudaDeviceSynchronize();
+  if (!h.empty()) cudaMemcpy(h.data(), t.dev, h.size() * 8, cudaMemcpyDeviceToHost);
+  FILE* f = std::fopen(path, "w");
+  if (!f) return;
+  auto st = [](unsigned long long v) { return v ? ~v : 0ull; };
+  for (int i = 0; i < t.next; ++i) {
+    const unsigned long long* w = h.data() + 8 * static_cast<size_t>(i);
+    std::fprintf(f, "{\"launch\":%d,\"first_start\":%llu,\"put_start\":%llu,\"put_end\":%llu,"
+                 "\"recv_start\":%llu,\"recv_ready\":%llu,\"recv_end\":%llu,\"end\":%llu,\"other_start\":%llu}\n",
+                 i, st(w[7]), st(w[0]), w[1], st(w[2]), w[3], w[4], w[5], st(w[6]));
+  }
+  std::fclose(f);
 }
 
 void launch_signal(unsigned long long* const* flag, unsigned long long* const* seq, int n, cudaStream_t s) {

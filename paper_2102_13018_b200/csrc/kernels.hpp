@@ -186,9 +186,18 @@ struct LaunchParams {
   unsigned long long* done_seq[kMaxPeers];
   int ndone = 0;
   int done_relaxed = 0;  // LL128 channels: acknowledge with a relaxed store
+  // Debug (SFG_TRACE_LAUNCHES): 8 words of %globaltimer marks for this
+  // launch (see kernels.cu trace_mark), nullptr otherwise.
+  unsigned long long* trace = nullptr;
   unsigned int* done_count = nullptr;
   FetchShuffle shuf;
 };
+
+// SFG_TRACE_LAUNCHES=N: per-launch timestamps of the first N launches of the
+// process (put / receive CTA start and end, data ready, launch end), dumped by
+// sfg_trace_dump. Debug only.
+unsigned long long* trace_slot();  // nullptr when tracing is off or full
+void trace_dump(const char* path);
 
 // Element type the kernel instantiates for.
 enum class ElemType : int32_t { u8, u16, u32, u64, i32, i64, f64 };

@@ -319,6 +319,7 @@ struct Launch {
     while (i < items.size()) {
       LaunchParams p{};
       std::copy(bufs, bufs + BUF_PEER0, p.bufs);
+      p.trace = trace_slot();
       p.bl = bl;
       p.wpv = static_cast<int64_t>(u.bytes() / 8);
       p.shuf = shuffle;
