@@ -195,6 +195,7 @@ sfg_comm make_comm(sfg_world world, int nranks, int rank, int device, const sfg:
   if (device >= 0) {
     SFG_CUDA(cudaSetDevice(device));
     SFG_CUDA(cudaFree(nullptr));  // create the context
+    sfg::trace_init();
   }
   if (cc.backend == "p2p") SFG_REQUIRE(device >= 0, "the p2p backend needs a device");
   // p2p: NCCL only carries the control plane (SetUp, slot mapping) when the

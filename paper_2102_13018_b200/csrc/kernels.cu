@@ -669,11 +669,11 @@ __device__ __forceinline__ void run_put_ll(const DSeg& s, const LaunchParams& P,
     a[u] = 0;
     b[u] = m;
     if (L < lines && w0 < W) {
-      const int64_t i = w0 / wpv;
+      const int64_t i = wpv == 1 ? w0 : w0 / wpv;
       a[u] = src[pat_index(s.src, i) * wpv + (w0 - i * wpv)];
     }
     if (L < lines && j != 7 && w0 + 1 < W) {
-      const int64_t i = (w0 + 1) / wpv;
+      const int64_t i = wpv == 1 ? w0 + 1 : (w0 + 1) / wpv;
       b[u] = src[pat_index(s.src, i) * wpv + (w0 + 1 - i * wpv)];
     }
   }
@@ -738,7 +738,7 @@ __device__ __forceinline__ void run_recv_ll(const DSeg& s, const PP& P, int64_t 
 #pragma unroll
       for (int t = 0; t < kEpw; ++t) {
         const int64_t e = w * kEpw + t;  // element index in the message
-        const int64_t i = e / bl;
+        const int64_t i = bl == 1 ? e : e / bl;
         const int64_t k = e - i * bl;
         T v;
         if constexpr (sizeof(T) == 8) {
@@ -1155,6 +1155,8 @@ TraceBuf& tbuf() {
   return t;
 }
 }  // namespace
+
+void trace_init() { (void)tbuf(); }
 
 unsigned long long* trace_slot() {
   TraceBuf& t = tbuf();

@@ -196,6 +196,7 @@ struct LaunchParams {
 // SFG_TRACE_LAUNCHES=N: per-launch timestamps of the first N launches of the
 // process (put / receive CTA start and end, data ready, launch end), dumped by
 // sfg_trace_dump. Debug only.
+void trace_init();                 // allocate the buffer (outside any capture)
 unsigned long long* trace_slot();  // nullptr when tracing is off or full
 void trace_dump(const char* path);
 
