@@ -183,3 +183,55 @@ def test_planner_matches_reference_two_sided():
         for r in range(nranks):
             assert [list(x) for x in got[r][0].root_ranks] == [list(x) for x in want[r][0]]
             assert [list(x) for x in got[r][0].leaf_ranks] == [list(x) for x in want[r][1]]
+
+
+def _relation_trial(t):
+    """selfcheck.cpp:243-283 shapes: random relations up to 8 ranks,
+    including empty and all-to-one relations."""
+    rng = graphs.Rng(graphs.mix_seed(t, 0x5D))
+    nranks = rng.range(1, 8)
+    kind = t % 4
+    specs = []
+    for r in range(nranks):
+        if kind == 0:  # empty relation
+            specs.append(sf.GraphSpec(rng.range(0, 5), 0))
+        elif kind == 1:  # all-to-one: every leaf on rank 0's roots
+            n = rng.range(0, 12)
+            specs.append(sf.GraphSpec(8 if r == 0 else 0, n, None, np.zeros(n, np.int32),
+                                      np.array([rng.bounded(8) for _ in range(n)], np.int64)))
+        else:
+            specs = graphs.random_graph_specs(9000 + t, nranks, 24)
+            break
+    return specs
+
+
+@pytest.mark.parametrize("t", range(24))
+def test_setup_duality_dense_vs_consensus(t):
+    """selfcheck.cpp:285-327 (SPEC.md acceptance 3): dense and consensus
+    discovery give identical TwoSidedInfo, and the (root rank, root offset,
+    leaf rank) edge multisets seen from the root side and from the leaf side
+    both equal the graph's."""
+    specs = _relation_trial(t)
+    n = len(specs)
+
+    def body(c):
+        a, b = sf.StarForest(c), sf.StarForest(c)
+        a.set_graph_spec(specs[c.rank()])
+        b.set_graph_spec(specs[c.rank()])
+        a.setup(sf.SetupAlg.dense)
+        b.setup(sf.SetupAlg.consensus)
+        return a.two_sided(), b.two_sided()
+
+    got = run_host(n, body)
+    from_root, from_leaf, from_graph = [], [], []
+    for q in range(n):
+        dense, cons = got[q]
+        assert dense == cons, q
+        spec = specs[q]
+        for rank, ords in dense.root_ranks:
+            from_root += [(rank, int(spec.remote_off[o]), q) for o in ords]
+        for rank, offs in dense.leaf_ranks:
+            from_leaf += [(q, int(o), rank) for o in offs]
+        from_graph += [(int(spec.remote_rank[o]), int(spec.remote_off[o]), q) for o in range(int(spec.nleaves))]
+    assert sorted(from_root) == sorted(from_graph)
+    assert sorted(from_leaf) == sorted(from_graph)
