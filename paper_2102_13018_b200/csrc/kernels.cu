@@ -704,42 +704,15 @@ __device__ __forceinline__ void run_recv_ll(const DSeg& s, const PP& P, int64_t 
   const int j = lane & 7;
   const int64_t L0 = blk * kLLLines + (threadIdx.x >> 5) * (4 * kLLIters) + (lane >> 3);
   if (__all_sync(0xffffffffu, L0 >= lines)) return;
-  unsigned long long a[kLLIters], b[kLLIters];
-  const unsigned long long t0 = global_ns();
-  for (;;) {
-    bool ok = true;
-#pragma unroll
-    for (int u = 0; u < kLLIters; ++u) {
-      const int64_t L = L0 + 4 * u;
-      a[u] = 0;
-      b[u] = m;
-      if (L < lines) ld_v2_volatile(reg + (s.ll_line + L) * 16 + 2 * j, a[u], b[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < kLLIters; ++u) {
-      const unsigned long long f = __shfl_sync(0xffffffffu, b[u], (lane & ~7) | 7);  // every lane
-      ok = ok && f == m;
-    }
-    if (__all_sync(0xffffffffu, ok)) break;
-    __nanosleep(20);
-    if (global_ns() - t0 > 30000000000ull) {
-      if (lane == 0) printf("sfgpu p2p: LL128 line never arrived (message %llu)\n", m);
-      __trap();
-    }
-  }
-  if constexpr (std::is_same_v<PP, LaunchParams>)
-    if (P.trace && lane == 0) atomicMax(P.trace + 3, global_ns());
   const int64_t bl = P.bl;
-#pragma unroll
-  for (int u = 0; u < kLLIters; ++u) {
-    const int64_t L = L0 + 4 * u;
-    if (L >= lines) break;
+  // Apply one line group's words to dst[pat(vertex)] (op; REPLACE copies).
+  auto apply = [&](int64_t L, unsigned long long a, unsigned long long b) {
     const int64_t w0 = L * 15 + 2 * j;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const int64_t w = w0 + q;
       if ((q == 1 && j == 7) || w >= W) break;
-      const unsigned long long word = q == 0 ? a[u] : b[u];
+      const unsigned long long word = q == 0 ? a : b;
 #pragma unroll
       for (int t = 0; t < kEpw; ++t) {
         const int64_t e = w * kEpw + t;  // element index in the message
@@ -759,7 +732,37 @@ __device__ __forceinline__ void run_recv_ll(const DSeg& s, const PP& P, int64_t 
           *d = apply_op<T, OP>(*d, v);
       }
     }
+  };
+  // Poll the warp's line groups; unpack each group as soon as all 4 of its
+  // lines carry flag m (warp-uniform decisions), re-read only the others.
+  unsigned pending = 0;
+#pragma unroll
+  for (int u = 0; u < kLLIters; ++u)
+    if (__any_sync(0xffffffffu, L0 + 4 * u < lines)) pending |= 1u << u;
+  const unsigned long long t0 = global_ns();
+  while (pending) {
+#pragma unroll
+    for (int u = 0; u < kLLIters; ++u) {
+      if (!((pending >> u) & 1u)) continue;
+      const int64_t L = L0 + 4 * u;
+      unsigned long long a = 0, b = m;
+      if (L < lines) ld_v2_volatile(reg + (s.ll_line + L) * 16 + 2 * j, a, b);
+      const unsigned long long f = __shfl_sync(0xffffffffu, b, (lane & ~7) | 7);  // every lane
+      if (__all_sync(0xffffffffu, f == m)) {
+        if (L < lines) apply(L, a, b);
+        pending &= ~(1u << u);
+      }
+    }
+    if (pending) {
+      __nanosleep(20);
+      if (global_ns() - t0 > 30000000000ull) {
+        if (lane == 0) printf("sfgpu p2p: LL128 line never arrived (message %llu)\n", m);
+        __trap();
+      }
+    }
   }
+  if constexpr (std::is_same_v<PP, LaunchParams>)
+    if (P.trace && lane == 0) atomicMax(P.trace + 3, global_ns());
 }
 
 // LL128 put completion: no flag (every line carries its own); the last CTA
