@@ -641,6 +641,12 @@ __device__ __forceinline__ void ld_v2_volatile(const unsigned long long* p, unsi
   asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // Message number of this CTA's segment: *counter + 1 (the counter advances
 // only after every CTA of the segment / launch has arrived).
 __device__ __forceinline__ unsigned long long ll_message(const unsigned long long* counter) {
@@ -657,7 +663,26 @@ __device__ __forceinline__ unsigned long long ll_message(const unsigned long lon
 // carries the flag m in word 15. All source loads of a thread are issued
 // before its stores.
 __device__ __forceinline__ void run_put_ll(const DSeg& s, const LaunchParams& P, int64_t blk) {
-  const unsigned long long m = ll_message(s.sig_seq);
+  // One thread reads the channel counter once, waits (relaxed polls: the
+  // lines carry their own validity) until the peer acknowledged message m-2,
+  // and publishes m to the CTA: a single barrier before the first store.
+  __shared__ unsigned long long msh;
+  if (threadIdx.x == 0) {
+    const unsigned long long seq = *s.sig_seq;
+    if (s.ll_credit != nullptr && seq >= 1) {
+      const unsigned long long t0 = global_ns();
+      while (ld_volatile_u64(s.ll_credit) + 1 < seq) {
+        __nanosleep(32);
+        if (global_ns() - t0 > 30000000000ull) {
+          printf("sfgpu p2p: LL128 credit stuck at %llu < %llu\n", ld_volatile_u64(s.ll_credit), seq - 1);
+          __trap();
+        }
+      }
+    }
+    msh = seq + 1;
+  }
+  __syncthreads();
+  const unsigned long long m = msh;
   const auto* src = static_cast<const unsigned long long*>(P.bufs[s.src_buf]);
   auto* dst = static_cast<unsigned long long*>(P.bufs[s.dst_buf]) + static_cast<int64_t>(m & 1) * s.ll_par;
   const int64_t wpv = P.wpv;

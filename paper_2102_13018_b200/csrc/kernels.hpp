@@ -142,6 +142,9 @@ struct DSeg {
   // (sent for puts, recvd for receives: message m = *sig_seq + 1).
   int64_t ll_line = 0;
   int64_t ll_par = 0;
+  // LL128 put: the peer's acknowledgement count for this channel; message m
+  // may overwrite parity m & 1 once it reaches m - 2.
+  const unsigned long long* ll_credit = nullptr;
 };
 
 // Wait until *flag >= *count + delta (count: a local message counter).

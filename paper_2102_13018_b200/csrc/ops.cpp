@@ -255,16 +255,18 @@ struct Launch {
 
   // LL128 put into a peer's region (see kernels.hpp): credit wait `wait`,
   // the channel's message counter `seq` (sent), its CTA counter `sig_count`.
-  void add_put_ll(const DPat& src, int sbuf, void* region, int64_t line, int64_t par, int64_t n, int wait,
-                  unsigned int* sig_count, unsigned long long* seq, bool remote, int64_t src_distinct = -1) {
+  void add_put_ll(const DPat& src, int sbuf, void* region, int64_t line, int64_t par, int64_t n,
+                  const unsigned long long* credit, unsigned int* sig_count, unsigned long long* seq, bool remote,
+                  int64_t src_distinct = -1) {
     DSeg s = pair_seg(src, sbuf, contig(0), BUF_PEER0, n, true);
     s.type = SEG_PUT_LL;
     s.run = 0;
     s.ll_line = line;
     s.ll_par = par;
+    s.ll_credit = credit;
     s.sig_count = sig_count;
     s.sig_seq = seq;
-    add(s, 0, src_distinct, -1, {wait});
+    add(s, 0, src_distinct, -1);
     items.back().peer = region;
     items.back().remote_put = remote;
   }
@@ -698,11 +700,11 @@ void add_puts_ll(OpHandle& h, Launch& L, const std::vector<DevPlan::Seg>& groups
     char* base = ps.base + (region == 0 ? 0 : region == 1 ? ps.root_at : ps.reply_at);
     const int64_t line = region == 1 ? ps.root_line : ps.leaf_line;
     SFG_REQUIRE(line >= 0, "p2p: peer slot has no group for this rank");
-    // message m goes to parity m & 1: the peer consumed message m-2 there
-    const int w = L.add_wait(s.free_flag(region, g.rank), s.sent(region, g.rank), -1);
-    L.add_put_ll(use_pat ? g.pat : contig(g.stage_off), sbuf, base, line, ps.par[region], g.n, w,
-                 s.seg_count(region, g.rank), s.sent(region, g.rank), g.rank != me,
-                 use_pat ? g.distinct : -1);
+    // message m goes to parity m & 1: the put kernel waits in-line until the
+    // peer consumed message m-2 there (its acknowledgement count)
+    L.add_put_ll(use_pat ? g.pat : contig(g.stage_off), sbuf, base, line, ps.par[region], g.n,
+                 s.free_flag(region, g.rank), s.seg_count(region, g.rank), s.sent(region, g.rank),
+                 g.rank != me, use_pat ? g.distinct : -1);
     if (g.rank != me) counters().bytes_sent += static_cast<uint64_t>(g.n) * ub;
     counters().pack_elided++;  // the put gathers straight from the caller's buffer
   }
