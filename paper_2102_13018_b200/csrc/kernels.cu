@@ -779,7 +779,7 @@ __device__ __forceinline__ void run_recv_ll(const DSeg& s, const PP& P, int64_t 
       }
     }
     if (pending) {
-      __nanosleep(20);
+      __nanosleep(P.ll_poll_ns);
       if (global_ns() - t0 > 30000000000ull) {
         if (lane == 0) printf("sfgpu p2p: LL128 line never arrived (message %llu)\n", m);
         __trap();

@@ -189,6 +189,7 @@ struct LaunchParams {
   unsigned long long* done_seq[kMaxPeers];
   int ndone = 0;
   int done_relaxed = 0;  // LL128 channels: acknowledge with a relaxed store
+  int ll_poll_ns = 20;   // LL128 receive: back-off between polls of unarrived lines
   // Debug (SFG_TRACE_LAUNCHES): 8 words of %globaltimer marks for this
   // launch (see kernels.cu trace_mark), nullptr otherwise.
   unsigned long long* trace = nullptr;

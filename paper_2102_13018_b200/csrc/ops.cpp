@@ -322,6 +322,11 @@ struct Launch {
       LaunchParams p{};
       std::copy(bufs, bufs + BUF_PEER0, p.bufs);
       p.trace = trace_slot();
+      static const int poll_ns = [] {
+        const char* e = std::getenv("SFG_LL_POLL_NS");
+        return e ? std::atoi(e) : 20;
+      }();
+      p.ll_poll_ns = poll_ns;
       p.bl = bl;
       p.wpv = static_cast<int64_t>(u.bytes() / 8);
       p.shuf = shuffle;

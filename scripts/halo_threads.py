@@ -36,7 +36,7 @@ def body(comm):
             sf.bcast_end(sf.bcast_begin(f, u, root, leaf, sf.ReduceOp.replace, st))
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=st):
+    with torch.cuda.graph(g, stream=st, capture_error_mode="thread_local"):
         for _ in range(K):
             sf.bcast_end(sf.bcast_begin(f, u, root, leaf, sf.ReduceOp.replace, st))
     torch.cuda.synchronize()

@@ -54,7 +54,15 @@ struct Chan {
   long long stage_words_per_parity;
   int nput;             // put CTAs (the rest receive)
   int verify;
+  u64* trace;           // optional: 8 words per launch (see ll128_body)
+  u64* trace_idx;       // launch counter (advanced by the last CTA)
 };
+
+__device__ __forceinline__ u64 gns() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ u64 ld_acq_sys(const u64* p) {
   u64 v;
@@ -132,7 +140,10 @@ __global__ void __launch_bounds__(256) flag_kernel(const __grid_constant__ Chan 
 // 2*(l%8), 2*(l%8)+1. IT line groups per warp (loads first, then stores).
 template <int IT, bool REL>
 __device__ __forceinline__ void ll128_body(const Chan& c) {
+  const u64 t_start = gns();
   __shared__ u64 sm;
+  __shared__ u64* tslot;
+  if (threadIdx.x == 0) tslot = c.trace ? c.trace + 8 * (*c.trace_idx % 4096) : nullptr;
   const int lines_per_cta = 8 * 4 * IT;
   const bool put = blockIdx.x < c.nput;
   if (threadIdx.x == 0) sm = put ? *c.sent + 1 : *c.recvd + 1;
@@ -161,6 +172,10 @@ __device__ __forceinline__ void ll128_body(const Chan& c) {
       if (L < c.lines) st_v2_vol(c.peer_stage + par + L * 16 + 2 * j, a[u], v[u]);
     }
     __syncthreads();
+    if (tslot && threadIdx.x == 0) {
+      atomicMax(tslot + 0, ~t_start);
+      atomicMax(tslot + 1, gns());
+    }
     if (threadIdx.x == 0 && arrive(c.put_count) + 1 == static_cast<unsigned>(c.nput)) {
       *c.put_count = 0;
       *c.sent = m;
@@ -184,6 +199,7 @@ __device__ __forceinline__ void ll128_body(const Chan& c) {
       if (__all_sync(0xffffffffu, ok)) break;
       __nanosleep(20);
     }
+    if (tslot && (threadIdx.x & 31) == 0) atomicMax(tslot + 3, gns());
 #pragma unroll
     for (int u = 0; u < IT; ++u) {
       const long long L = L0 + 4 * u;
@@ -200,9 +216,14 @@ __device__ __forceinline__ void ll128_body(const Chan& c) {
     }
   }
   __syncthreads();
+  if (tslot && threadIdx.x == 0) atomicMax(tslot + 4, gns());
   if (threadIdx.x == 0 && arrive(c.all_count) + 1 == gridDim.x) {
     *c.all_count = 0;
     *c.recvd = m;
+    if (tslot) {
+      atomicMax(tslot + 5, gns());
+      *c.trace_idx = *c.trace_idx + 1;
+    }
     if (REL)
       st_rel_sys(c.peer_free, m);
     else
@@ -362,6 +383,50 @@ int main(int argc, char** argv) {
       const double us = t[t.size() / 2];
       std::printf("{\"test\":\"exchange\",\"proto\":\"%s\",\"bytes\":%lld,\"us\":%.2f,\"GBps\":%.1f,\"ctas\":%d}\n",
                   pname[proto], bytes, us, bytes / (us * 1e-6) / 1e9, 2 * c[0].nput);
+    }
+  }
+  // 3. timeline of 20 exchanges at 2 MB (proto ll128), globaltimer marks
+  {
+    reset();
+    const long long n = (2ll << 20) / 8;
+    u64 *tr[2], *ti[2];
+    for (int d = 0; d < 2; ++d) {
+      CK(cudaSetDevice(d));
+      CK(cudaMalloc(&tr[d], 4096 * 64));
+      CK(cudaMemset(tr[d], 0, 4096 * 64));
+      CK(cudaMalloc(&ti[d], 8));
+      CK(cudaMemset(ti[d], 0, 8));
+    }
+    Chan c[2] = {chan(0, n, 0, 1), chan(1, n, 0, 1)};
+    for (int d = 0; d < 2; ++d) {
+      c[d].trace = tr[d];
+      c[d].trace_idx = ti[d];
+    }
+    cudaGraphExec_t ge[2];
+    for (int d = 0; d < 2; ++d) {
+      CK(cudaSetDevice(d));
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(D[d].s, cudaStreamCaptureModeThreadLocal));
+      for (int k = 0; k < 20; ++k) launch(d, c[d], 1);
+      CK(cudaStreamEndCapture(D[d].s, &g));
+      CK(cudaGraphInstantiate(&ge[d], g, 0));
+    }
+    for (int d = 0; d < 2; ++d) {
+      CK(cudaSetDevice(d));
+      CK(cudaGraphLaunch(ge[d], D[d].s));
+    }
+    for (int d = 0; d < 2; ++d) {
+      CK(cudaSetDevice(d));
+      CK(cudaDeviceSynchronize());
+      std::vector<u64> h(20 * 8);
+      CK(cudaMemcpy(h.data(), tr[d], h.size() * 8, cudaMemcpyDeviceToHost));
+      const u64 t0 = ~h[0];
+      for (int k = 0; k < 20; ++k) {
+        const u64* w = h.data() + 8 * k;
+        std::printf("{\"trace\":%d,\"launch\":%d,\"put_start\":%.2f,\"put_end\":%.2f,\"recv_ready\":%.2f,\"cta_end\":%.2f,\"end\":%.2f}\n",
+                    d, k, (double)(~w[0] - t0) / 1e3, (double)(w[1] - t0) / 1e3, (double)(w[3] - t0) / 1e3,
+                    (double)(w[4] - t0) / 1e3, (double)(w[5] - t0) / 1e3);
+      }
     }
   }
   return 0;

@@ -2,7 +2,8 @@
 // roots) through the Blackwell TMA row gather (cp.async.bulk.tensor.2d ...
 // tile::gather4) instead of LSU loads: the roots are viewed as a 2-D tensor of
 // 16-byte rows (2 roots per row); one instruction fetches 4 rows into shared
-// memory, completion on an mbarrier; the CTA then picks each leaf's half of
+// memory (32-byte rows of 4 roots: one 128-byte aligned slot per gather4),
+// completion on an mbarrier; the CTA then picks each leaf's half of
 // its row and stores the tile coalesced. Compared with the LSU gather on the
 // same data (cold L2: 256 MB read-flush before every call).
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tma_gather_bench tma_gather_bench.cu
@@ -36,8 +37,8 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __global__ void __launch_bounds__(kThr) gather_tma(const __grid_constant__ CUtensorMap tmap, const int* __restrict__ idx,
                                                    double* __restrict__ leaf, long long L) {
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* rows = reinterpret_cast<uint64_t*>(smem);                   // kStages x kT x 2 words
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kStages * kT * 16);  // kStages mbarriers
+  uint64_t* rows = reinterpret_cast<uint64_t*>(smem);                   // kStages x kT x 4 words
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kStages * kT * 32);  // kStages mbarriers
   const long long ntiles = (L + kT - 1) / kT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid < kStages) {
@@ -54,7 +55,7 @@ __global__ void __launch_bounds__(kThr) gather_tma(const __grid_constant__ CUten
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     const uint32_t b = smem_u32(bar + st);
     if (lane == 0)
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kT * 16) : "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kT * 32) : "memory");
     __syncwarp();
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -62,12 +63,12 @@ __global__ void __launch_bounds__(kThr) gather_tma(const __grid_constant__ CUten
       int r[4];
       if (i0 + 3 < L) {
         const int4 v = __ldg(reinterpret_cast<const int4*>(idx + i0));
-        r[0] = v.x >> 1; r[1] = v.y >> 1; r[2] = v.z >> 1; r[3] = v.w >> 1;
+        r[0] = v.x >> 2; r[1] = v.y >> 2; r[2] = v.z >> 2; r[3] = v.w >> 2;
       } else {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) r[u] = i0 + u < L ? (__ldg(idx + i0 + u) >> 1) : 0;
+        for (int u = 0; u < 4; ++u) r[u] = i0 + u < L ? (__ldg(idx + i0 + u) >> 2) : 0;
       }
-      const uint32_t dst = smem_u32(rows + (size_t(st) * kT + q * 128 + lane * 4) * 2);
+      const uint32_t dst = smem_u32(rows + (size_t(st) * kT + q * 128 + lane * 4) * 4);
       asm volatile(
           "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
           " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
@@ -92,14 +93,14 @@ __global__ void __launch_bounds__(kThr) gather_tma(const __grid_constant__ CUten
           : "r"(b), "r"(phase[st])
           : "memory");
     phase[st] ^= 1u;
-    const uint64_t* tile = rows + size_t(st) * kT * 2;
+    const uint64_t* tile = rows + size_t(st) * kT * 4;
 #pragma unroll
     for (int j = 0; j < kT / kThr; ++j) {
       const int e = j * kThr + tid;
       const long long i = t * kT + e;
       if (i < L) {
-        const int half = __ldg(idx + i) & 1;
-        leaf[i] = __longlong_as_double(static_cast<long long>(tile[e * 2 + half]));
+        const int q4 = __ldg(idx + i) & 3;
+        leaf[i] = __longlong_as_double(static_cast<long long>(tile[e * 4 + q4]));
       }
     }
     __syncthreads();  // stage st consumed
@@ -164,9 +165,9 @@ int main() {
   cudaDriverEntryPointQueryResult q;
   CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q));
   CUtensorMap tmap;
-  const cuuint64_t gdim[2] = {2, static_cast<cuuint64_t>(R / 2)};
-  const cuuint64_t gstride[1] = {16};
-  const cuuint32_t box[2] = {2, 1};
+  const cuuint64_t gdim[2] = {4, static_cast<cuuint64_t>(R / 4)};
+  const cuuint64_t gstride[1] = {32};
+  const cuuint32_t box[2] = {4, 1};
   const cuuint32_t estr[2] = {1, 1};
   CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, droot, gdim, gstride, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -175,7 +176,7 @@ int main() {
     std::printf("{\"error\":\"cuTensorMapEncodeTiled %d\"}\n", static_cast<int>(cr));
     return 1;
   }
-  const size_t smem = kStages * kT * 16 + kStages * 8;
+  const size_t smem = kStages * kT * 32 + kStages * 8;
   CK(cudaFuncSetAttribute(gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   std::vector<double> got(L);
   cudaEvent_t e0, e1;
@@ -205,7 +206,7 @@ int main() {
   CK(cudaMemset(dleaf, 0, L * 8));
   float us = timeit([&] { gather_elem<<<(L + 2047) / 2048, 256>>>(droot, didx, dleaf, L); });
   std::printf("{\"kernel\":\"lsu_elem8\",\"us\":%.2f,\"ok\":%s}\n", us, check() ? "true" : "false");
-  for (int per_sm : {1, 2, 3}) {
+  for (int per_sm : {1}) {
     CK(cudaMemset(dleaf, 0, L * 8));
     us = timeit([&] { gather_tma<<<148 * per_sm, kThr, smem>>>(tmap, didx, dleaf, L); });
     CK(cudaGetLastError());
