@@ -15,6 +15,7 @@
 //   scatter:  /root/reference/proj/src/pack.cpp:220-256
 //   fetch:    /root/reference/proj/src/ops.cpp:110-158, 521-563
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -1176,7 +1177,8 @@ void batched(unsigned long long* const* flag, unsigned long long* const* seq, in
 namespace {
 struct TraceBuf {
   unsigned long long* dev = nullptr;
-  int cap = 0, next = 0;
+  int cap = 0;
+  std::atomic<int> next{0};  // thread ranks launch concurrently
   TraceBuf() {
     const char* e = std::getenv("SFG_TRACE_LAUNCHES");
     cap = e ? std::atoi(e) : 0;
@@ -1196,20 +1198,22 @@ void trace_init() { (void)tbuf(); }
 
 unsigned long long* trace_slot() {
   TraceBuf& t = tbuf();
-  if (t.cap == 0 || t.next >= t.cap) return nullptr;
-  return t.dev + 8 * static_cast<size_t>(t.next++);
+  if (t.cap == 0) return nullptr;
+  const int k = t.next.fetch_add(1);
+  return k < t.cap ? t.dev + 8 * static_cast<size_t>(k) : nullptr;
 }
 
 void trace_dump(const char* path) {
   TraceBuf& t = tbuf();
   if (t.cap == 0) return;
-  std::vector<unsigned long long> h(static_cast<size_t>(t.next) * 8);
+  const int used = std::min(t.next.load(), t.cap);
+  std::vector<unsigned long long> h(static_cast<size_t>(used) * 8);
   cudaDeviceSynchronize();
   if (!h.empty()) cudaMemcpy(h.data(), t.dev, h.size() * 8, cudaMemcpyDeviceToHost);
   FILE* f = std::fopen(path, "w");
   if (!f) return;
   auto st = [](unsigned long long v) { return v ? ~v : 0ull; };
-  for (int i = 0; i < t.next; ++i) {
+  for (int i = 0; i < used; ++i) {
     const unsigned long long* w = h.data() + 8 * static_cast<size_t>(i);
     std::fprintf(f, "{\"launch\":%d,\"first_start\":%llu,\"put_start\":%llu,\"put_end\":%llu,"
                  "\"recv_start\":%llu,\"recv_ready\":%llu,\"recv_end\":%llu,\"end\":%llu,\"other_start\":%llu}\n",
