@@ -766,16 +766,24 @@ __device__ __forceinline__ void run_recv_ll(const DSeg& s, const PP& P, int64_t 
   for (int u = 0; u < kLLIters; ++u)
     if (__any_sync(0xffffffffu, L0 + 4 * u < lines)) pending |= 1u << u;
   const unsigned long long t0 = global_ns();
+  unsigned long long a[kLLIters], b[kLLIters];
   while (pending) {
+    // all pending loads in flight at once (one L2 round trip per poll) ...
+#pragma unroll
+    for (int u = 0; u < kLLIters; ++u) {
+      const int64_t L = L0 + 4 * u;
+      a[u] = 0;
+      b[u] = m;
+      if (((pending >> u) & 1u) && L < lines) ld_v2_volatile(reg + (s.ll_line + L) * 16 + 2 * j, a[u], b[u]);
+    }
+    // ... then every group whose 4 lines all carry m is unpacked at once
 #pragma unroll
     for (int u = 0; u < kLLIters; ++u) {
       if (!((pending >> u) & 1u)) continue;
-      const int64_t L = L0 + 4 * u;
-      unsigned long long a = 0, b = m;
-      if (L < lines) ld_v2_volatile(reg + (s.ll_line + L) * 16 + 2 * j, a, b);
-      const unsigned long long f = __shfl_sync(0xffffffffu, b, (lane & ~7) | 7);  // every lane
+      const unsigned long long f = __shfl_sync(0xffffffffu, b[u], (lane & ~7) | 7);  // every lane
       if (__all_sync(0xffffffffu, f == m)) {
-        if (L < lines) apply(L, a, b);
+        const int64_t L = L0 + 4 * u;
+        if (L < lines) apply(L, a[u], b[u]);
         pending &= ~(1u << u);
       }
     }
