@@ -684,8 +684,12 @@ __device__ __forceinline__ void run_put_ll(const DSeg& s, const LaunchParams& P,
   }
   __syncthreads();
   const unsigned long long m = msh;
+  // descriptor fields in registers (the shared-memory copy is re-read after
+  // every volatile store otherwise)
+  const DPat sp = s.src;
   const auto* src = static_cast<const unsigned long long*>(P.bufs[s.src_buf]);
-  auto* dst = static_cast<unsigned long long*>(P.bufs[s.dst_buf]) + static_cast<int64_t>(m & 1) * s.ll_par;
+  auto* dst = static_cast<unsigned long long*>(P.bufs[s.dst_buf]) + static_cast<int64_t>(m & 1) * s.ll_par +
+              s.ll_line * 16;
   const int64_t wpv = P.wpv;
   const int64_t W = s.n * wpv;
   const int64_t lines = (W + 14) / 15;
@@ -699,19 +703,25 @@ __device__ __forceinline__ void run_put_ll(const DSeg& s, const LaunchParams& P,
     const int64_t w0 = L * 15 + 2 * j;
     a[u] = 0;
     b[u] = m;
+    if (sp.kind == PAT_CONTIG) {  // the common case: one contiguous run of words
+      const unsigned long long* base = src + sp.start * wpv;
+      if (L < lines && w0 < W) a[u] = base[w0];
+      if (L < lines && j != 7 && w0 + 1 < W) b[u] = base[w0 + 1];
+      continue;
+    }
     if (L < lines && w0 < W) {
       const int64_t i = wpv == 1 ? w0 : w0 / wpv;
-      a[u] = src[pat_index(s.src, i) * wpv + (w0 - i * wpv)];
+      a[u] = src[pat_index(sp, i) * wpv + (w0 - i * wpv)];
     }
     if (L < lines && j != 7 && w0 + 1 < W) {
       const int64_t i = wpv == 1 ? w0 + 1 : (w0 + 1) / wpv;
-      b[u] = src[pat_index(s.src, i) * wpv + (w0 + 1 - i * wpv)];
+      b[u] = src[pat_index(sp, i) * wpv + (w0 + 1 - i * wpv)];
     }
   }
 #pragma unroll
   for (int u = 0; u < kLLIters; ++u) {
     const int64_t L = L0 + 4 * u;
-    if (L < lines) st_v2_volatile(dst + (s.ll_line + L) * 16 + 2 * j, a[u], b[u]);
+    if (L < lines) st_v2_volatile(dst + L * 16 + 2 * j, a[u], b[u]);
   }
 }
 
@@ -720,7 +730,9 @@ __device__ __forceinline__ void run_put_ll(const DSeg& s, const LaunchParams& P,
 template <class T, int OP, class PP = LaunchParams>
 __device__ __forceinline__ void run_recv_ll(const DSeg& s, const PP& P, int64_t blk) {
   const unsigned long long m = ll_message(s.sig_seq);
-  const auto* reg = static_cast<const unsigned long long*>(P.bufs[s.src_buf]) + static_cast<int64_t>(m & 1) * s.ll_par;
+  const DPat dp = s.dst;
+  const auto* reg = static_cast<const unsigned long long*>(P.bufs[s.src_buf]) + static_cast<int64_t>(m & 1) * s.ll_par +
+                    s.ll_line * 16;
   T* dst = static_cast<T*>(P.bufs[s.dst_buf]);
   constexpr int kEpw = 8 / static_cast<int>(sizeof(T));  // elements per word
   const int64_t wpv = P.wpv;
@@ -751,7 +763,7 @@ __device__ __forceinline__ void run_recv_ll(const DSeg& s, const PP& P, int64_t 
           const uint32_t part = static_cast<uint32_t>(word >> (32 * t));
           v = *reinterpret_cast<const T*>(&part);
         }
-        T* d = dst + pat_index(s.dst, i) * bl + k;
+        T* d = dst + pat_index(dp, i) * bl + k;
         if constexpr (OP == OP_REPLACE)
           *d = v;
         else
@@ -774,7 +786,7 @@ __device__ __forceinline__ void run_recv_ll(const DSeg& s, const PP& P, int64_t 
       const int64_t L = L0 + 4 * u;
       a[u] = 0;
       b[u] = m;
-      if (((pending >> u) & 1u) && L < lines) ld_v2_volatile(reg + (s.ll_line + L) * 16 + 2 * j, a[u], b[u]);
+      if (((pending >> u) & 1u) && L < lines) ld_v2_volatile(reg + L * 16 + 2 * j, a[u], b[u]);
     }
     // ... then every group whose 4 lines all carry m is unpacked at once
 #pragma unroll
