@@ -923,15 +923,24 @@ void begin_leaf_to_root(OpHandle& h) {
   if (h.coupled_split)
     for (auto& it : local.items) it.seg.skip_dst = d.coupled_bits;
   if (ll) {
-    // incoming contributions are copied out of the LL lines into the plain
-    // root stage in the put launch (acknowledged there); End folds them
+    // Incoming contributions are copied out of the LL lines into the plain
+    // root stage in the put launch (acknowledged there); End folds them.
+    // Without self edges and with at most one remote contribution per root
+    // (a halo), the order of application is immaterial: the put launch
+    // applies them straight to rootdata and End only joins.
     const bool self_group = has_self_group(h, d.lg);
     h.fused_unpack = false;
+    h.ll_direct = false;
+    const bool direct = !d.has_self && !d.remote_root_dups && !self_group;
     auto fuse = [&](Launch& L) {
       if (self_group) return;
-      add_recvs_ll(h, L, d.lg, 1, [](const DevPlan::Seg& g) { return contig(g.stage_off); },
-                   BUF_ROOT_STAGE, true);
+      if (direct)
+        add_recvs_ll(h, L, d.lg, 1, [](const DevPlan::Seg& g) { return g.pat; }, BUF_ROOT, replace);
+      else
+        add_recvs_ll(h, L, d.lg, 1, [](const DevPlan::Seg& g) { return contig(g.stage_off); },
+                     BUF_ROOT_STAGE, true);
       h.fused_unpack = true;
+      h.ll_direct = direct;
     };
     p2p_begin(h, pack, local, fuse);
     return;
@@ -965,6 +974,10 @@ void end_leaf_to_root(OpHandle& h) {
   auto wait_k = [&bits](size_t k) { return bits.empty() ? std::vector<int>{} : std::vector<int>{bits[k]}; };
   Comm& c = sf.comm();
   const bool ll = use_ll(h);
+  if (ll && h.ll_direct) {  // applied in the put launch
+    p2p_join(h);
+    return;
+  }
   if (ll && !h.fused_unpack) {
     // self group (force_remote): copy the LL messages out here, behind Begin
     Launch R;

@@ -561,6 +561,7 @@ struct OpHandle {
   std::vector<XferOp> reply_recvs;  // fetch-and-op replies
   bool forked = false;              // p2p: the puts ran on the comm stream
   bool fused_unpack = false;        // p2p Bcast: the unpack ran in the put launch
+  bool ll_direct = false;           // p2p Reduce: remote contributions applied in the put launch
   bool coupled_split = false;       // reduce: coupled roots folded in End (DevPlan::coupled_bits)
   std::vector<uint8_t> zero_copy_recv;
   std::vector<int32_t> fetch_order;  // free-order fetch: group order used (empty: stored order)
