@@ -324,3 +324,37 @@ def test_p2p_puts_never_stage_on_the_sender():
     cleaves = rank_data(ctl, 1, np.int64, 1, 200, "leaf")
     c = _counted(ctl, "reduce", [cleaves, croots], "sum", "p2p", 2)
     assert c["pack_copies"] == 0 and c["pack_elided"] > 0, c
+
+
+@need2
+@pytest.mark.parametrize("dtype,bl", [(np.int32, 2), (np.int32, 3), (np.int32, 4), (np.uint8, 16), (np.uint8, 5)])
+def test_p2p_protocol_per_unit_size(dtype, bl):
+    """The p2p slot protocol follows the unit size: whole 8-byte words ->
+    LL128 lines (int32 x 2 / x 4: two elements per word; 16 opaque bytes),
+    other sizes -> the flag protocol (int32 x 3, 5 opaque bytes). Both
+    bit-exact against the oracle between GPUs."""
+    n = min(ngpu(), 4)
+    specs = graphs.random_graph_specs(61, n, 60)
+    roots = rank_data(specs, 4, dtype, bl, 100, "root")
+    leaves = rank_data(specs, 4, dtype, bl, 200, "leaf")
+    cfg = lambda: sf.CommConfig(backend="p2p")  # noqa: E731
+    out = run_gpu(specs, "bcast", [roots, leaves], blocklen=bl, config=cfg(), devices=list(range(n)))
+    assert_same(out[1], O.bcast(specs, roots, leaves, "replace", bl))
+    if dtype != np.uint8:
+        out = run_gpu(specs, "bcast", [roots, leaves], op="max", blocklen=bl, config=cfg(), devices=list(range(n)))
+        assert_same(out[1], O.bcast(specs, roots, leaves, "max", bl))
+        out = run_gpu(specs, "reduce", [leaves, roots], op="sum", blocklen=bl, config=cfg(), devices=list(range(n)))
+        assert_same(out[1], O.reduce(specs, leaves, roots, "sum", bl))
+        upd = [np.zeros_like(x) for x in leaves]
+        r, _, u = run_gpu(specs, "fetch_and_op", [roots, leaves, upd], op="sum", blocklen=bl, config=cfg(),
+                          devices=list(range(n)))
+        orr, ou = O.fetch_and_op(specs, roots, leaves, upd, "sum", bl)
+        assert_same(r, orr)
+        assert_same(u, ou)
+    deg = O.degrees(specs)
+    multi = [np.zeros(int(d.sum()) * bl, dtype) for d in deg]
+    out = run_gpu(specs, "gather", [leaves, multi], blocklen=bl, config=cfg(), devices=list(range(n)))
+    og = O.gather(specs, leaves, bl)
+    assert_same(out[1], og)
+    out = run_gpu(specs, "scatter", [og, leaves], blocklen=bl, config=cfg(), devices=list(range(n)))
+    assert_same(out[1], O.scatter(specs, og, leaves, bl))
