@@ -496,11 +496,23 @@ __device__ __forceinline__ void run_csr_warp(const DSeg& s, const LaunchParams& 
     if (lo >= hi) return;
     const int64_t ro = static_cast<int64_t>(__ldg(s.csr_roots + r)) * bl + k;
     if (fetch && P.shuf.n > 1) {
+      // group boundaries in one coalesced pass over the root's entries:
+      // bound[g] = lo + #entries of a group < g (entries ascend by group)
+      int32_t bound[kMaxShuffle + 1];
+#pragma unroll
+      for (int g = 0; g <= kMaxShuffle; ++g) bound[g] = lo;
+      for (int32_t c = lo; c < hi; c += 32) {
+        const int32_t j = c + lane;
+        const int gj = j < hi ? shuf_group(P.shuf, __ldg(s.csr_ent + j)) : kMaxShuffle;
+#pragma unroll
+        for (int g = 1; g <= kMaxShuffle; ++g)
+          bound[g] += __popc(__ballot_sync(0xffffffffu, gj < g));
+      }
       T acc = root[ro];
       for (int q = 0; q < P.shuf.n; ++q) {
         const int g = P.shuf.perm[q];
-        const int32_t a = shuf_bound(P.shuf, s.csr_ent, lo, hi, g);
-        const int32_t b = shuf_bound(P.shuf, s.csr_ent, a, hi, g + 1);
+        const int32_t a = bound[g];
+        const int32_t b = g + 1 < P.shuf.n ? bound[g + 1] : hi;
         if (a < b) acc = csr_warp_range<T, OP>(s, leaf, stage, aux, bl, k, a, b, acc, true);
       }
       if (lane == 0) root[ro] = acc;

@@ -163,10 +163,12 @@ DSeg csr_seg(const DevPlan& d, CsrRange range, int32_t type, bool seq, size_t ub
     const char* e = std::getenv("SFG_CSR_WARP_LIMIT");
     return e ? std::atoll(e) : int64_t(32768);
   }();
-  // Deterministic float fetches (sequential order kept through shuffles)
-  // too, when SFG_CSR_WARP_SEQ is set (ablation, measured at N=2/4).
-  static const bool warp_seq = std::getenv("SFG_CSR_WARP_SEQ") != nullptr;
-  const bool warp_fetch = type == SEG_CSR_FETCH && (!seq || warp_seq) && s.n < warp_limit;
+  // Deterministic float fetches too, keeping the exact sequential order
+  // through shuffles: config 4 at N=4 (16,384 roots per rank) FetchAndOp f64
+  // 309 -> 256 us (profiles/r2_cfg4_n4*.log); SFG_CSR_NO_WARP_SEQ restores
+  // thread per root for them.
+  static const bool no_warp_seq = std::getenv("SFG_CSR_NO_WARP_SEQ") != nullptr;
+  const bool warp_fetch = type == SEG_CSR_FETCH && (!seq || !no_warp_seq) && s.n < warp_limit;
   if (s.n >= 8192 && !warp_fetch) s.csr_warp = 0;
   return s;
 }
