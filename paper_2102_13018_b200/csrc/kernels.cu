@@ -847,7 +847,15 @@ template <class T, int OP, int MODE>
 __global__ void __launch_bounds__(kThreads, MODE == 0 ? 4 : MODE == 1 ? 3 : 2)
     segments_kernel(const __grid_constant__ LaunchParams P) {
   constexpr bool FULL = MODE == 1;
-  const int64_t b = blockIdx.x;
+  int64_t b = blockIdx.x;
+  if (P.ilv_a > 0) {  // interleave group A (puts, local) with group B (receives)
+    const int64_t na = P.ilv_a, nb = static_cast<int64_t>(gridDim.x) - na;
+    const int64_t m = na < nb ? na : nb;
+    if (b < 2 * m)
+      b = (b & 1) ? na + (b >> 1) : (b >> 1);
+    else
+      b = na > nb ? b - m : b;  // the rest of the larger group, in order
+  }
   const unsigned long long t_start = P.trace ? global_ns() : 0;
   int s = 0;
   while (s + 1 < P.nseg && b >= P.block_start[s + 1]) ++s;
@@ -1148,6 +1156,16 @@ int launch_segments(LaunchParams& p, ElemType t, int op, cudaStream_t stream) {
   p.nseg = n;
   p.block_start[n] = blocks;
   if (blocks == 0) return 0;
+  if (p.ilv_a < 0) {
+    p.ilv_a = 0;
+    for (int s = 1; s < n; ++s)
+      if (p.seg[s].type == SEG_RECV_LL) {
+        bool tail = true;  // receives must be the trailing segments
+        for (int t = s; t < n; ++t) tail = tail && p.seg[t].type == SEG_RECV_LL;
+        if (tail) p.ilv_a = p.block_start[s];
+        break;
+      }
+  }
   p.bldiv = make_fastdiv(static_cast<uint32_t>(p.bl > 0x7fffffff ? 1 : p.bl));
   bool ok = false;
   switch (t) {

@@ -190,6 +190,12 @@ struct LaunchParams {
   int ndone = 0;
   int done_relaxed = 0;  // LL128 channels: acknowledge with a relaxed store
   int ll_poll_ns = 20;   // LL128 receive: back-off between polls of unarrived lines
+  // LL128 launches: CTAs of the receive segments (the trailing ones) are
+  // dispatched interleaved with the put / local CTAs instead of after them,
+  // so large messages are unpacked while they stream in. ilv_a = number of
+  // blocks before the first receive segment (0 = off); launch_segments sets
+  // it when requested with -1.
+  int64_t ilv_a = 0;
   // Debug (SFG_TRACE_LAUNCHES): 8 words of %globaltimer marks for this
   // launch (see kernels.cu trace_mark), nullptr otherwise.
   unsigned long long* trace = nullptr;

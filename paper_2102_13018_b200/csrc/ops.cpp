@@ -199,6 +199,7 @@ struct Launch {
   void* bufs[BUF_PEER0] = {};
   FetchShuffle shuffle;
   bool done_relaxed = false;  // LL128 acknowledgements (kernels.cu st_relaxed_sys)
+  bool interleave = false;    // LL128: dispatch receive CTAs among the put CTAs
   bool any_op = false;
   const char* tag = "kernel";
 
@@ -327,6 +328,7 @@ struct Launch {
       LaunchParams p{};
       std::copy(bufs, bufs + BUF_PEER0, p.bufs);
       p.trace = trace_slot();
+      p.ilv_a = interleave ? -1 : 0;
       static const int poll_ns = [] {
         const char* e = std::getenv("SFG_LL_POLL_NS");
         return e ? std::atoi(e) : 20;
@@ -739,6 +741,7 @@ void add_recvs_ll(OpHandle& h, Launch& L, const std::vector<DevPlan::Seg>& group
     L.add(sg, 0, -1, g.distinct);
     L.add_done(s.peer_free_flag(region, g.rank, me), s.recvd(region, g.rank), s.done_count);
     L.done_relaxed = true;
+    L.interleave = true;
     counters().bytes_recv += static_cast<uint64_t>(g.n) * h.unit.bytes();
     counters().unpack_copies++;
   }
