@@ -755,19 +755,41 @@ __device__ __forceinline__ void run_recv_ll(const DSeg& s, const PP& P, int64_t 
   const int64_t L0 = blk * kLLLines + (threadIdx.x >> 5) * (4 * kLLIters) + (lane >> 3);
   if (__all_sync(0xffffffffu, L0 >= lines)) return;
   const int64_t bl = P.bl;
-  // Apply one line group's words to dst[pat(vertex)] (op; REPLACE copies).
-  auto apply = [&](int64_t L, unsigned long long a, unsigned long long b) {
-    const int64_t w0 = L * 15 + 2 * j;
+  // Destination of every element this lane may receive, computed before the
+  // data arrives (2 words per line group, kEpw elements per word); for a
+  // reduction the old values are loaded up front too, so applying a line
+  // group that lands costs no further memory round trip.
+  constexpr int kE = kLLIters * 2 * kEpw;
+  T* dptr[kE];
+  T old[kE];
+#pragma unroll
+  for (int u = 0; u < kLLIters; ++u) {
+    const int64_t w0 = (L0 + 4 * u) * 15 + 2 * j;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const int64_t w = w0 + q;
-      if ((q == 1 && j == 7) || w >= W) break;
-      const unsigned long long word = q == 0 ? a : b;
+      const bool valid = L0 + 4 * u < lines && !(q == 1 && j == 7) && w < W;
 #pragma unroll
       for (int t = 0; t < kEpw; ++t) {
+        const int x = (u * 2 + q) * kEpw + t;
+        dptr[x] = nullptr;
+        if (!valid) continue;
         const int64_t e = w * kEpw + t;  // element index in the message
         const int64_t i = bl == 1 ? e : e / bl;
         const int64_t k = e - i * bl;
+        dptr[x] = dst + pat_index(dp, i) * bl + k;
+        if constexpr (OP != OP_REPLACE) old[x] = *dptr[x];
+      }
+    }
+  }
+  auto apply = [&](int u, unsigned long long a, unsigned long long b) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const unsigned long long word = q == 0 ? a : b;
+#pragma unroll
+      for (int t = 0; t < kEpw; ++t) {
+        const int x = (u * 2 + q) * kEpw + t;
+        if (dptr[x] == nullptr) continue;
         T v;
         if constexpr (sizeof(T) == 8) {
           v = *reinterpret_cast<const T*>(&word);
@@ -775,11 +797,10 @@ __device__ __forceinline__ void run_recv_ll(const DSeg& s, const PP& P, int64_t 
           const uint32_t part = static_cast<uint32_t>(word >> (32 * t));
           v = *reinterpret_cast<const T*>(&part);
         }
-        T* d = dst + pat_index(dp, i) * bl + k;
         if constexpr (OP == OP_REPLACE)
-          *d = v;
+          *dptr[x] = v;
         else
-          *d = apply_op<T, OP>(*d, v);
+          *dptr[x] = apply_op<T, OP>(old[x], v);
       }
     }
   };
@@ -806,8 +827,7 @@ __device__ __forceinline__ void run_recv_ll(const DSeg& s, const PP& P, int64_t 
       if (!((pending >> u) & 1u)) continue;
       const unsigned long long f = __shfl_sync(0xffffffffu, b[u], (lane & ~7) | 7);  // every lane
       if (__all_sync(0xffffffffu, f == m)) {
-        const int64_t L = L0 + 4 * u;
-        if (L < lines) apply(L, a[u], b[u]);
+        apply(u, a[u], b[u]);
         pending &= ~(1u << u);
       }
     }
