@@ -351,11 +351,13 @@ __device__ __forceinline__ void run_csr_t(const DSeg& s, const PP& P, int64_t bl
     if (t0 >= total) return;
     int64_t r, k;
     im.split(t0, r, k);
-    if (skipped(s.skip_dst, __ldg(s.csr_roots + r))) return;
+    // root id and entry range loaded together (one memory round trip)
+    const int32_t rid = __ldg(s.csr_roots + r);
     const int32_t lo = __ldg(s.csr_lo + r);
     const int32_t hi = __ldg(s.csr_hi + r);
+    if (skipped(s.skip_dst, rid)) return;
     if (lo >= hi) return;
-    const int64_t ro = static_cast<int64_t>(__ldg(s.csr_roots + r)) * bl + k;
+    const int64_t ro = static_cast<int64_t>(rid) * bl + k;
     if (FETCH && P.shuf.n > 1) {
       T acc = root[ro];
       for (int q = 0; q < P.shuf.n; ++q) {
@@ -490,11 +492,13 @@ __device__ __forceinline__ void run_csr_warp(const DSeg& s, const LaunchParams& 
     if (w0 >= items) return;
     int64_t r, k;
     im.split(w0, r, k);
-    if (skipped(s.skip_dst, __ldg(s.csr_roots + r))) return;
+    // root id and entry range loaded together (one memory round trip)
+    const int32_t rid = __ldg(s.csr_roots + r);
     const int32_t lo = __ldg(s.csr_lo + r);
     const int32_t hi = __ldg(s.csr_hi + r);
+    if (skipped(s.skip_dst, rid)) return;
     if (lo >= hi) return;
-    const int64_t ro = static_cast<int64_t>(__ldg(s.csr_roots + r)) * bl + k;
+    const int64_t ro = static_cast<int64_t>(rid) * bl + k;
     if (fetch && P.shuf.n > 1) {
       // group boundaries in one coalesced pass over the root's entries:
       // bound[g] = lo + #entries of a group < g (entries ascend by group)
