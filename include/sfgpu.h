@@ -125,6 +125,10 @@ int sfg_comm_create_ext(int nranks, int rank, int device, const char* backend,
                         sfg_comm* out);
 int sfg_comm_destroy(sfg_comm c);
 int sfg_comm_rank(sfg_comm c, int* rank, int* size, int* device);
+/* Host allgather over the communicator's control plane (the reference's
+ * Comm::allgather / allreduce building block, comm.hpp:118-127): `out`
+ * receives size * bytes, rank r's `in` at r * bytes. Collective. */
+int sfg_comm_allgather(sfg_comm c, const void* in, size_t bytes, void* out);
 
 /* sf::StarForest(Comm) (starforest.hpp:64) */
 int sfg_sf_create(sfg_comm c, sfg_sf* out);

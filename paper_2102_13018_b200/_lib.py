@@ -89,6 +89,7 @@ _SIGS = {
                                       C.POINTER(_V)]),
     "sfg_comm_destroy": (C.c_int, [_V]),
     "sfg_comm_rank": (C.c_int, [_V, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "sfg_comm_allgather": (C.c_int, [_V, _V, C.c_size_t, _V]),
     "sfg_sf_create": (C.c_int, [_V, C.POINTER(_V)]),
     "sfg_sf_destroy": (C.c_int, [_V]),
     "sfg_sf_set_graph": (C.c_int, [_V, C.c_int64, C.c_int64, _V, _V, _V]),

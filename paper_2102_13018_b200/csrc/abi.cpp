@@ -267,6 +267,13 @@ int sfg_comm_rank(sfg_comm c, int* rank, int* size, int* device) {
   });
 }
 
+int sfg_comm_allgather(sfg_comm c, const void* in, size_t bytes, void* out) {
+  return guard([&] {
+    SFG_REQUIRE(c != nullptr, "allgather needs a valid communicator");
+    c->c->ctrl().allgather(in, bytes, out);
+  });
+}
+
 int sfg_sf_create(sfg_comm c, sfg_sf* out) {
   return guard([&] {
     SFG_REQUIRE(c != nullptr, "star forest needs a valid communicator");

@@ -259,6 +259,15 @@ class Comm:
     def rank(self) -> int:
         return self._rank
 
+    def allgather_int64(self, values) -> np.ndarray:
+        """Every rank's int64 vector (same length on every rank), stacked
+        (size x n) — the control plane's allgather. Collective."""
+        v = np.ascontiguousarray(np.asarray(values, dtype=np.int64).reshape(-1))
+        out = np.zeros((self._size, v.size), np.int64)
+        _check(_lib().sfg_comm_allgather(self._h, v.ctypes.data if v.size else None, v.nbytes,
+                                         out.ctypes.data if out.size else None))
+        return out
+
     def size(self) -> int:
         return self._size
 

@@ -152,6 +152,31 @@ def build_column_sf(comm, col_layout: Layout, global_cols) -> StarForest:
     return f
 
 
+def select_submatrix_columns(sf_a: StarForest, sf_b: StarForest, selected_global_columns,
+                             stream=None):
+    """spmv.cpp:45-73 (collective): the new column index, in the
+    submatrix's column layout (my selected columns take [prefix, prefix +
+    count), ranks in order), of every leaf of `sf_a` (the matrix's column SF,
+    e.g. build_column_sf over its garray), or -1 for a column nobody
+    selected. `sf_b` = build_column_sf over the selection. Two device
+    operations: Reduce REPLACE of the new indices onto the column owners, then
+    Bcast REPLACE of the owners' tags into sf_a's leaves. Returns an int64
+    CUDA tensor of sf_a.leaf_index_bound() entries."""
+    import torch
+
+    comm = sf_a.comm
+    sel = np.asarray(selected_global_columns, dtype=np.int64)
+    counts = comm.allgather_int64([sel.size])[:, 0]
+    prefix = int(counts[:comm.rank()].sum())
+    new_index = torch.arange(prefix, prefix + sel.size, dtype=torch.int64, device="cuda")
+    tags = torch.full((sf_b.nroots(),), -1, dtype=torch.int64, device="cuda")
+    u = _sf.Unit(Kind.int64)
+    _sf.reduce(sf_b, u, new_index, tags, _sf.ReduceOp.replace, stream)
+    out = torch.full((sf_a.leaf_index_bound(),), -1, dtype=torch.int64, device="cuda")
+    _sf.bcast(sf_a, u, tags, out, _sf.ReduceOp.replace, stream)
+    return out
+
+
 def build_ghost_sf(comm, m: SplitMatrix) -> StarForest:
     """spmv.hpp:140-143."""
     return build_column_sf(comm, m.col_layout, m.garray)

@@ -88,3 +88,14 @@ def test_two_process_gloo_setup_matches_in_process(tmp_path):
         assert norm(got[q]["rand"]) == norm(want_rand[q])
         assert set(got[q]["g2l"][4]) <= {"contiguous", "affine"}
         assert got[q]["max"] == 2.0
+
+
+def test_control_plane_allgather_threads():
+    """sfg_comm_allgather over the in-process control plane (host-only ranks)."""
+    from paper_2102_13018_b200 import sf
+
+    def body(c):
+        return c.allgather_int64([c.rank() * 10, c.rank() + 1]).tolist()
+
+    got = sf.run_ranks(sf.CommConfig(nranks=3), body, devices=[-1] * 3)
+    assert all(g == [[0, 1], [10, 2], [20, 3]] for g in got)

@@ -76,3 +76,44 @@ def test_mismatched_blocks_rejected():
         return True
 
     assert all(sf.run_ranks(sf.CommConfig(nranks=2), body))
+
+
+def _selection_trial(t, seed=1):
+    """selfcheck.cpp:765-797 draw for draw (Rng(mix_seed(seed + t*911, 0x77))):
+    4 ranks, 8-40 columns, random reduced column lists, disjoint selections
+    (trial 0 selects everything); oracle = position in rank-then-list order."""
+    from paper_2102_13018_b200 import graphs
+
+    rng = graphs.Rng(graphs.mix_seed(seed + t * 911, 0x77))
+    nranks = 4
+    ncols = rng.range(8, 40)
+    garray = [[c for c in range(ncols) if rng.chance(0.4)] for _ in range(nranks)]
+    selected = [[] for _ in range(nranks)]
+    for c in range(ncols):
+        if t != 0 and rng.chance(0.4):
+            continue
+        selected[rng.bounded(nranks)].append(c)
+    new_index, nxt = {}, 0
+    for r in range(nranks):
+        for c in selected[r]:
+            new_index[c] = nxt
+            nxt += 1
+    return S.Layout.contiguous(ncols, nranks), garray, selected, new_index
+
+
+@pytest.mark.parametrize("t", range(20))
+def test_select_submatrix_columns(t):
+    """SPEC.md acceptance 9 / selfcheck submatrix_selection: a Reduce REPLACE
+    + Bcast REPLACE composition over two column forests on the device."""
+    layout, garray, selected, new_index = _selection_trial(t)
+
+    def body(comm):
+        r = comm.rank()
+        sf_a = S.build_column_sf(comm, layout, garray[r])
+        sf_b = S.build_column_sf(comm, layout, selected[r])
+        return S.select_submatrix_columns(sf_a, sf_b, selected[r]).cpu().numpy()
+
+    got = sf.run_ranks(sf.CommConfig(nranks=4), body)
+    for r in range(4):
+        want = [new_index.get(c, -1) for c in garray[r]]
+        assert got[r].tolist() == want, (t, r)
