@@ -358,3 +358,57 @@ def test_p2p_protocol_per_unit_size(dtype, bl):
     assert_same(out[1], og)
     out = run_gpu(specs, "scatter", [og, leaves], blocklen=bl, config=cfg(), devices=list(range(n)))
     assert_same(out[1], O.scatter(specs, og, leaves, bl))
+
+
+@need2
+def test_p2p_random_delays_every_iteration_checked():
+    """SPEC.md acceptance 5 (one-sided protocol safety): many Bcast + Reduce
+    rounds over the LL128 p2p path with random delays injected on every rank
+    — host sleeps before Begin and device-side spin kernels before the put
+    launch (torch.cuda._sleep) — so messages, credits and acknowledgements
+    arrive in every relative order; each round's leaves and roots are checked
+    on the device against the oracle's values for that round."""
+    import random
+    import time
+
+    import torch
+
+    n = min(ngpu(), 4)
+    specs = graphs.random_graph_specs(77, n, 80)
+    roots = rank_data(specs, 6, np.float64, 1, 100, "root")
+    leaves0 = [np.zeros(s.leaf_bound()) for s in specs]
+    want_leaf = O.bcast(specs, roots, leaves0)
+    u = sf.Unit(sf.Kind.float64)
+    iters = 200
+
+    def body(comm):
+        r = comm.rank()
+        rnd = random.Random(1000 + r)
+        f = sf.StarForest(comm)
+        f.set_graph_spec(specs[r])
+        f.setup()
+        st = torch.cuda.Stream()
+        base = torch.from_numpy(roots[r]).cuda()
+        wl = torch.from_numpy(want_leaf[r]).cuda()
+        root = torch.empty_like(base)
+        leaf = torch.zeros(max(1, specs[r].leaf_bound()), dtype=torch.float64, device="cuda")[:specs[r].leaf_bound()]
+        bad = torch.zeros((), dtype=torch.int64, device="cuda")
+        torch.cuda.synchronize()
+        with torch.cuda.stream(st):
+            for it in range(1, iters + 1):
+                if rnd.random() < 0.3:
+                    time.sleep(rnd.random() * 1e-3)
+                root.copy_(base * it)
+                if rnd.random() < 0.5:
+                    torch.cuda._sleep(rnd.randrange(1, 400000))
+                sf.bcast_end(sf.bcast_begin(f, u, root, leaf, sf.ReduceOp.replace, st))
+                if leaf.numel():
+                    bad += (leaf != wl * it).sum()
+                if rnd.random() < 0.5:
+                    torch.cuda._sleep(rnd.randrange(1, 400000))
+                sf.reduce_end(sf.reduce_begin(f, u, leaf, root, sf.ReduceOp.replace, st))
+        st.synchronize()
+        return int(bad.item())
+
+    got = sf.run_ranks(sf.CommConfig(nranks=n, backend="p2p"), body, devices=list(range(n)))
+    assert got == [0] * n
