@@ -238,28 +238,6 @@ __device__ __forceinline__ void run_pair_rows(const DSeg& s, const PP& P, int64_
   }
 }
 
-// en[q] = ent[j + q] for j + q < hi (0 beyond). For 8 entries well inside the
-// range, three aligned 16-byte loads replace eight 4-byte ones (a
-// high-degree root's entries are contiguous; it never reads past hi + 3).
-template <int kB>
-__device__ __forceinline__ void load_entries(const int32_t* ent, int32_t j, int32_t hi, int32_t (&en)[kB]) {
-  if constexpr (kB == 8) {
-    if (j + 12 <= hi) {
-      const int a = j & 3;
-      const int4* p = reinterpret_cast<const int4*>(ent + (j - a));
-      if ((reinterpret_cast<uintptr_t>(ent) & 15) == 0) {
-        const int4 v0 = __ldg(p), v1 = __ldg(p + 1), v2 = __ldg(p + 2);
-        const int32_t w[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
-#pragma unroll
-        for (int q = 0; q < 8; ++q) en[q] = a == 0 ? w[q] : a == 1 ? w[q + 1] : a == 2 ? w[q + 2] : w[q + 3];
-        return;
-      }
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < kB; ++q) en[q] = j + q < hi ? __ldg(ent + j + q) : 0;
-}
-
 // Root-sorted fold in the reference order (self leaves ascending, then remote
 // groups ascending rank, each in ascending leaf order). Sequential per root,
 // so floating-point results are bit-identical to the CPU reference.
@@ -299,7 +277,8 @@ __device__ __forceinline__ T csr_thread_range(const DSeg& s, const T* leaf, T* s
   // waits on one memory round trip (its values) instead of two (entries,
   // then values): config 4 Reduce 164 -> 112 us.
   int32_t en[kB];
-  load_entries<kB>(s.csr_ent, lo, hi, en);
+#pragma unroll
+  for (int q = 0; q < kB; ++q) en[q] = lo + q < hi ? __ldg(s.csr_ent + lo + q) : 0;
   for (int32_t j = lo; j < hi; j += kB) {
     T c[kB];
 #pragma unroll
@@ -308,7 +287,8 @@ __device__ __forceinline__ T csr_thread_range(const DSeg& s, const T* leaf, T* s
         c[q] = en[q] >= 0 ? leaf[static_cast<int64_t>(en[q]) * bl + k]
                           : stage[static_cast<int64_t>(-en[q] - 1) * bl + k];
     int32_t nx[kB];
-    load_entries<kB>(s.csr_ent, j + kB, hi, nx);
+#pragma unroll
+    for (int q = 0; q < kB; ++q) nx[q] = j + kB + q < hi ? __ldg(s.csr_ent + j + kB + q) : 0;
 #pragma unroll
     for (int q = 0; q < kB; ++q) {
       if (j + q >= hi) break;
