@@ -628,6 +628,8 @@ struct DevMatrix {
     int32_t* row_len = nullptr;
     int32_t* col = nullptr;
     void* val = nullptr;
+    int64_t n_nz_rows = 0;        // rows with at least one entry
+    int32_t* nz_rows = nullptr;   // their indices, ascending
   };
   int device = -1;
   Kind kind = Kind::float64;

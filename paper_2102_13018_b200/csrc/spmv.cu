@@ -75,6 +75,45 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t rows, const int6
   y[r] = ADD ? add_rn(y[r], acc) : acc;
 }
 
+// y[r] += B_r . x over the rows that HAVE entries only (list nz_rows). For
+// the other rows the reference adds an empty dot product, y[r] + 0, which
+// leaves every y the diagonal product can produce unchanged bit for bit: its
+// accumulator starts at +0.0 and round-to-nearest never yields -0.0 from it,
+// so y is never -0.0 (the one value + 0 changes), and integers are unchanged.
+template <class T>
+__global__ void __launch_bounds__(256) sell_spmv_add_rows_kernel(int64_t n, const int32_t* __restrict__ rows,
+                                                                 const int64_t* __restrict__ slice_off,
+                                                                 const int32_t* __restrict__ row_len,
+                                                                 const int32_t* __restrict__ col,
+                                                                 const T* __restrict__ val,
+                                                                 const T* __restrict__ x, T* __restrict__ y) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t r = __ldg(rows + t);
+  const int64_t base = __ldg(slice_off + (r >> 5)) + (r & 31);
+  const int len = __ldg(row_len + r);
+  T acc = T(0);
+  int k = 0;
+  for (; k + 4 <= len; k += 4) {
+    int32_t c[4];
+    T v[4], xv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      c[q] = __ldg(col + base + static_cast<int64_t>(k + q) * 32);
+      v[q] = __ldg(val + base + static_cast<int64_t>(k + q) * 32);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) xv[q] = __ldg(x + c[q]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc = add_rn(acc, mul_rn(v[q], xv[q]));
+  }
+  for (; k < len; ++k) {
+    const int64_t e = base + static_cast<int64_t>(k) * 32;
+    acc = add_rn(acc, mul_rn(__ldg(val + e), __ldg(x + __ldg(col + e))));
+  }
+  y[r] = add_rn(y[r], acc);
+}
+
 // Host SELL-32 image of a CSR matrix (rows sliced by 32, column-major inside
 // a slice; padding slots are never read).
 struct SellHost {
@@ -150,7 +189,39 @@ void upload_sell(const SellHost& h, size_t esz, DevMatrix::Sell& d, std::vector<
   d.col = static_cast<int32_t*>(up(h.col.data(), h.col.size() * sizeof(int32_t)));
   d.val = up(h.val.data(), h.val.size());
   d.slots = static_cast<int64_t>(h.col.size());
+  std::vector<int32_t> nz;
+  for (size_t r = 0; r < h.row_len.size(); ++r)
+    if (h.row_len[r] > 0) nz.push_back(static_cast<int32_t>(r));
+  d.n_nz_rows = static_cast<int64_t>(nz.size());
+  d.nz_rows = static_cast<int32_t*>(up(nz.data(), nz.size() * sizeof(int32_t)));
   (void)esz;
+}
+
+// y += B lvec over B's non-empty rows only (see sell_spmv_add_rows_kernel):
+// valid when y holds a product this library computed (never -0.0).
+template <class T>
+void launch_add_rows(const DevMatrix::Sell& m, const void* x, void* y, cudaStream_t s) {
+  if (m.n_nz_rows == 0) return;
+  const unsigned blocks = static_cast<unsigned>((m.n_nz_rows + 255) / 256);
+  const bool timed = timing_enabled();
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timed) {
+    e0 = timing_event();
+    e1 = timing_event();
+    SFG_CUDA(cudaEventRecord(e0, s));
+  }
+  sell_spmv_add_rows_kernel<T><<<blocks, 256, 0, s>>>(m.n_nz_rows, m.nz_rows, m.slice_off, m.row_len, m.col,
+                                                      static_cast<const T*>(m.val), static_cast<const T*>(x),
+                                                      static_cast<T*>(y));
+  SFG_CUDA(cudaGetLastError());
+  counters().kernel_launches++;
+  if (timed) {
+    SFG_CUDA(cudaEventRecord(e1, s));
+    const double nnz = static_cast<double>(m.nnz);
+    const double b = nnz * (sizeof(T) + 4) + static_cast<double>(m.cols) * sizeof(T) +
+                     static_cast<double>(m.n_nz_rows) * (sizeof(T) * 2 + 8);
+    timing_record("spmv_offdiag", e0, e1, b);
+  }
 }
 
 template <class T, bool ADD, bool PLUS_ZERO>
@@ -239,7 +310,12 @@ void spmv(StarForest& sf, const DevMatrix& diag, const DevMatrix& off, const voi
   else
     run_sell<false>(diag.kind, diag.fwd, x_owned, y, s);
   bcast_end(*h);
-  if (off.nnz != 0) run_sell<true>(off.kind, off.fwd, lvec, y, s);
+  if (off.nnz != 0) {
+    if (off.kind == Kind::float64)
+      launch_add_rows<double>(off.fwd, lvec, y, s);
+    else
+      launch_add_rows<int64_t>(off.fwd, lvec, y, s);
+  }
 }
 
 // spmv.hpp:161-169
