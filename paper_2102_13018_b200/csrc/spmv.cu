@@ -21,6 +21,10 @@
 
 #include "sfg.hpp"
 
+#ifndef SPMV_UNROLL
+#define SPMV_UNROLL 8
+#endif
+
 namespace sfg {
 namespace {
 
@@ -39,6 +43,46 @@ __device__ __forceinline__ T add_rn(T a, T b) {
     return static_cast<T>(static_cast<unsigned long long>(a) + static_cast<unsigned long long>(b));
 }
 
+// acc += sum_k val * x[col] over one row's SELL slots, in CSR order. The
+// matrix streams through once (evict-first loads keep L1 for x); kUnroll
+// slots' loads are issued before their products so a thread keeps 2*kUnroll
+// independent loads in flight.
+constexpr int kUnroll = SPMV_UNROLL;
+template <class T>
+__device__ __forceinline__ void row_dot(int64_t base, int len, const int32_t* __restrict__ col,
+                                        const T* __restrict__ val, const T* __restrict__ x, T& acc) {
+  int k = 0;
+  for (; k + kUnroll <= len; k += kUnroll) {
+    int32_t c[kUnroll];
+    T v[kUnroll], xv[kUnroll];
+#pragma unroll
+    for (int q = 0; q < kUnroll; ++q) {
+      c[q] = __ldcs(col + base + static_cast<int64_t>(k + q) * 32);
+      v[q] = __ldcs(val + base + static_cast<int64_t>(k + q) * 32);
+    }
+#pragma unroll
+    for (int q = 0; q < kUnroll; ++q) xv[q] = __ldg(x + c[q]);
+#pragma unroll
+    for (int q = 0; q < kUnroll; ++q) acc = add_rn(acc, mul_rn(v[q], xv[q]));
+  }
+  if (k < len) {  // the tail, as one predicated batch
+    int32_t c[kUnroll];
+    T v[kUnroll], xv[kUnroll];
+#pragma unroll
+    for (int q = 0; q < kUnroll; ++q)
+      if (k + q < len) {
+        c[q] = __ldcs(col + base + static_cast<int64_t>(k + q) * 32);
+        v[q] = __ldcs(val + base + static_cast<int64_t>(k + q) * 32);
+      }
+#pragma unroll
+    for (int q = 0; q < kUnroll; ++q)
+      if (k + q < len) xv[q] = __ldg(x + c[q]);
+#pragma unroll
+    for (int q = 0; q < kUnroll; ++q)
+      if (k + q < len) acc = add_rn(acc, mul_rn(v[q], xv[q]));
+  }
+}
+
 // y[r] (=|+=) sum_k vals * x[col], k in the row's CSR order.
 template <class T, bool ADD, bool PLUS_ZERO>
 __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t rows, const int64_t* __restrict__ slice_off,
@@ -53,24 +97,7 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t rows, const int6
   const int64_t base = __ldg(slice_off + s) + lane;
   const int len = __ldg(row_len + r);
   T acc = T(0);
-  int k = 0;
-  for (; k + 4 <= len; k += 4) {
-    int32_t c[4];
-    T v[4], xv[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      c[q] = __ldg(col + base + static_cast<int64_t>(k + q) * 32);
-      v[q] = __ldg(val + base + static_cast<int64_t>(k + q) * 32);
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) xv[q] = __ldg(x + c[q]);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc = add_rn(acc, mul_rn(v[q], xv[q]));
-  }
-  for (; k < len; ++k) {
-    const int64_t e = base + static_cast<int64_t>(k) * 32;
-    acc = add_rn(acc, mul_rn(__ldg(val + e), __ldg(x + __ldg(col + e))));
-  }
+  row_dot(base, len, col, val, x, acc);
   if constexpr (PLUS_ZERO) acc = add_rn(acc, T(0));
   y[r] = ADD ? add_rn(y[r], acc) : acc;
 }
@@ -93,24 +120,7 @@ __global__ void __launch_bounds__(256) sell_spmv_add_rows_kernel(int64_t n, cons
   const int64_t base = __ldg(slice_off + (r >> 5)) + (r & 31);
   const int len = __ldg(row_len + r);
   T acc = T(0);
-  int k = 0;
-  for (; k + 4 <= len; k += 4) {
-    int32_t c[4];
-    T v[4], xv[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      c[q] = __ldg(col + base + static_cast<int64_t>(k + q) * 32);
-      v[q] = __ldg(val + base + static_cast<int64_t>(k + q) * 32);
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) xv[q] = __ldg(x + c[q]);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc = add_rn(acc, mul_rn(v[q], xv[q]));
-  }
-  for (; k < len; ++k) {
-    const int64_t e = base + static_cast<int64_t>(k) * 32;
-    acc = add_rn(acc, mul_rn(__ldg(val + e), __ldg(x + __ldg(col + e))));
-  }
+  row_dot(base, len, col, val, x, acc);
   y[r] = add_rn(y[r], acc);
 }
 
