@@ -281,6 +281,8 @@ std::unique_ptr<DevMatrix> matrix_upload(Comm& comm, int64_t rows, int64_t cols,
                                          const int64_t* colind, const void* vals, Kind kind) {
   SFG_REQUIRE(kind == Kind::float64 || kind == Kind::int64, "SpMV supports float64 and int64 matrices");
   SFG_REQUIRE(rows >= 0 && cols >= 0 && rowptr != nullptr && rowptr[0] == 0, "matrix: bad CSR row pointer");
+  // row numbers (of the matrix and of its transpose) are int32 on the device
+  SFG_REQUIRE(rows <= INT32_MAX && cols <= INT32_MAX, "matrix dimensions outside the int32 range");
   for (int64_t r = 0; r < rows; ++r) SFG_REQUIRE(rowptr[r + 1] >= rowptr[r], "matrix: bad CSR row pointer");
   const int64_t nnz = rowptr[rows];
   for (int64_t i = 0; i < nnz; ++i)
