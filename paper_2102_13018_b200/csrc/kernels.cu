@@ -18,6 +18,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <type_traits>
 
@@ -1181,12 +1182,24 @@ int launch_segments(LaunchParams& p, ElemType t, int op, cudaStream_t stream) {
   p.block_start[n] = blocks;
   if (blocks == 0) return 0;
   if (p.ilv_a < 0) {
+    // Only when the CTAs ahead of the receives are streaming work (no
+    // indexed gather or scatter): receive CTAs that spin among put CTAs doing
+    // random gathers take SM slots those gathers need (config 4 at N=4:
+    // Reduce 143 -> 174 us with interleaving), while structured puts finish
+    // at the rate the link drains them anyway.
+    static const int mode = [] {
+      const char* e = std::getenv("SFG_LL_INTERLEAVE");  // ablation: "all" | "none"
+      return e == nullptr ? 0 : std::strcmp(e, "all") == 0 ? 1 : std::strcmp(e, "none") == 0 ? 2 : 0;
+    }();
     p.ilv_a = 0;
-    for (int s = 1; s < n; ++s)
+    for (int s = 1; s < n && mode != 2; ++s)
       if (p.seg[s].type == SEG_RECV_LL) {
-        bool tail = true;  // receives must be the trailing segments
-        for (int t = s; t < n; ++t) tail = tail && p.seg[t].type == SEG_RECV_LL;
-        if (tail) p.ilv_a = p.block_start[s];
+        bool ok = true;  // receives must be the trailing segments
+        for (int t = s; t < n; ++t) ok = ok && p.seg[t].type == SEG_RECV_LL;
+        for (int t = 0; t < s && mode == 0; ++t)
+          ok = ok && (p.seg[t].type == SEG_PUT_LL || p.seg[t].type == SEG_PAIR) &&
+               p.seg[t].src.kind != PAT_INDEXED && p.seg[t].dst.kind != PAT_INDEXED;
+        if (ok) p.ilv_a = p.block_start[s];
         break;
       }
   }
