@@ -449,6 +449,16 @@ void dev_narrow_index(const int64_t* src, int64_t n, int32_t* dst) {
   SFG_REQUIRE(read1(sc.v) == ~0ull, "index exceeds the int32 range of device plans");
 }
 
+bool dev_keys_sorted(const int64_t* items, const int64_t* src, int64_t n) {
+  if (n <= 1) return true;
+  Scratch sc;
+  const int64_t bad = src == nullptr
+                          ? find_first(n - 1, [=] __device__(int64_t i) { return items[i] > items[i + 1]; }, sc)
+                          : find_first(
+                                n - 1, [=] __device__(int64_t i) { return src[items[i]] > src[items[i + 1]]; }, sc);
+  return bad == n - 1;
+}
+
 bool dev_any_repeat(const std::vector<std::pair<const int64_t*, int64_t>>& lists, int64_t bound) {
   if (bound <= 0) return false;
   Scratch sc;

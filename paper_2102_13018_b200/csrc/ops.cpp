@@ -169,7 +169,14 @@ DSeg csr_seg(const DevPlan& d, CsrRange range, int32_t type, bool seq, size_t ub
   // thread per root for them.
   static const bool no_warp_seq = std::getenv("SFG_CSR_NO_WARP_SEQ") != nullptr;
   const bool warp_fetch = type == SEG_CSR_FETCH && (!seq || !no_warp_seq) && s.n < warp_limit;
-  if (s.n >= 8192 && !warp_fetch) s.csr_warp = 0;
+  // End's order-free folds (integers, free-order floats) over the roots that
+  // receive remote contributions (every root of a rank in config 4 at N>1,
+  // ~256 contributions each) likewise: config 4 Reduce at N=4 143 -> 125 us.
+  // The exact-order float fold stays thread per root there (warp: 149 us).
+  static const bool no_warp_end = std::getenv("SFG_CSR_NO_WARP_END") != nullptr;  // ablation
+  const bool warp_end =
+      type == SEG_CSR_FOLD && range == CsrRange::remote_only && !no_warp_end && !seq && s.n < warp_limit;
+  if (s.n >= 8192 && !warp_fetch && !warp_end) s.csr_warp = 0;
   return s;
 }
 

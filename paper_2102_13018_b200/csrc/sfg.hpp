@@ -536,6 +536,11 @@ class StarForest {
   std::unique_ptr<StarForest> multi_;
   std::unique_ptr<DevPlan> dev_;
   std::vector<std::unique_ptr<Staging>> staging_;
+  // Message order of the remote groups (build_wire_order): the group itself
+  // when its items already travel in root order, else a re-sorted copy.
+  std::vector<const Group*> wire_rg_, wire_lg_;
+  std::vector<std::unique_ptr<Group>> wire_store_;
+  void build_wire_order(bool self);
 };
 
 bool stream_capturing(cudaStream_t s);
@@ -605,6 +610,8 @@ void dev_csr_fill(const int64_t* keys, const int64_t* vals, int64_t n, int64_t b
 struct DevPlan;
 void dev_build_csr(DevPlan& d, int32_t* key, int32_t* val, int64_t total, int64_t n_self, int64_t nroots,
                    int64_t leaf_bound, bool self);
+// Whether keys never decrease: items[i] (src == nullptr) or src[items[i]].
+bool dev_keys_sorted(const int64_t* items, const int64_t* src, int64_t n);
 // Whether any value in [0, bound) occurs twice across the lists.
 bool dev_any_repeat(const std::vector<std::pair<const int64_t*, int64_t>>& lists, int64_t bound);
 

@@ -401,6 +401,75 @@ StarForest& StarForest::multi_sf() {
 
 // ------------------------------------------------------------ device plan
 
+// Message order. Inside each remote group the items travel sorted (stably)
+// by root offset rather than in the leaf rank's leaf order. Both sides derive
+// the same permutation from the same keys (the root offsets: the leaf side
+// from its graph, the root side from its group), so nothing is exchanged;
+// every root's contributions keep their relative (reference) order, so folds
+// and fetch-and-op serializations are unchanged bit for bit; and the root
+// side receives each root's contributions from a group back to back, so its
+// fold reads the stage in runs instead of at random. Groups whose items are
+// already in root order (halo faces, ghost columns) are used as they are.
+// The group plans the API exposes keep the reference's order.
+void StarForest::build_wire_order(bool self) {
+  static const bool off = std::getenv("SFG_NO_WIRE_SORT") != nullptr;  // ablation
+  wire_rg_.clear();
+  wire_lg_.clear();
+  wire_store_.clear();
+  const size_t s0 = self ? 1 : 0;
+  // Device-set graphs are checked on the device; host copies are made only
+  // when some group needs re-sorting.
+  if (!off && dg_ && !dg_->host_ready) {
+    bool all_sorted = true;
+    for (size_t gi = s0; gi < root_groups_.size() && all_sorted; ++gi)
+      all_sorted = dev_keys_sorted(root_groups_[gi].ditems, dg_->off, root_groups_[gi].count());
+    for (size_t gi = s0; gi < leaf_groups_.size() && all_sorted; ++gi)
+      all_sorted = dev_keys_sorted(leaf_groups_[gi].ditems, nullptr, leaf_groups_[gi].count());
+    if (!all_sorted) host_graph();
+  }
+  const bool host = !dg_ || dg_->host_ready;
+  auto wire = [&](const Group& g, bool leaf_side) -> const Group* {
+    const int64_t n = g.count();
+    if (off || !host || n <= 1) return &g;  // !host: every group checked sorted above
+    auto key = [&](int64_t i) {
+      const int64_t it = g.items[static_cast<size_t>(i)];
+      return leaf_side ? remote_off_of(it) : it;
+    };
+    bool sorted = true;
+    int64_t kmax = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t k = key(i);
+      if (i > 0 && key(i - 1) > k) sorted = false;
+      kmax = std::max(kmax, k);
+    }
+    if (sorted) return &g;
+    std::vector<int64_t> perm(static_cast<size_t>(n));
+    if (kmax <= 4 * n + 4096) {  // stable counting sort
+      std::vector<int64_t> at(static_cast<size_t>(kmax) + 2, 0);
+      for (int64_t i = 0; i < n; ++i) ++at[static_cast<size_t>(key(i)) + 1];
+      std::partial_sum(at.begin(), at.end(), at.begin());
+      for (int64_t i = 0; i < n; ++i) perm[static_cast<size_t>(at[static_cast<size_t>(key(i))]++)] = i;
+    } else {
+      std::iota(perm.begin(), perm.end(), int64_t(0));
+      std::stable_sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) { return key(a) < key(b); });
+    }
+    auto p = std::make_unique<Group>();
+    p->rank = g.rank;
+    p->items.resize(static_cast<size_t>(n));
+    HostVec<int64_t> idx(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t it = g.items[static_cast<size_t>(perm[static_cast<size_t>(i)])];
+      p->items[static_cast<size_t>(i)] = it;
+      idx[static_cast<size_t>(i)] = leaf_side ? leaf_index(it) : it;
+    }
+    p->pat = Pattern::analyze(idx.data(), n);
+    wire_store_.push_back(std::move(p));
+    return wire_store_.back().get();
+  };
+  for (size_t gi = s0; gi < root_groups_.size(); ++gi) wire_rg_.push_back(wire(root_groups_[gi], true));
+  for (size_t gi = s0; gi < leaf_groups_.size(); ++gi) wire_lg_.push_back(wire(leaf_groups_[gi], false));
+}
+
 DevPlan& StarForest::dev() {
   require_state(SfState::set_up, "device plan");
   if (dev_ && dev_->built) return *dev_;
@@ -422,12 +491,13 @@ DevPlan& StarForest::dev() {
   };
 
   const bool self = self_first_ && !force;
+  build_wire_order(self);
   if (self) {
     reserve_pat(leaf_groups_.front().pat);
     reserve_pat(root_groups_.front().pat);
   }
-  for (size_t gi = self ? 1 : 0; gi < root_groups_.size(); ++gi) reserve_pat(root_groups_[gi].pat);
-  for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size(); ++gi) reserve_pat(leaf_groups_[gi].pat);
+  for (const Group* g : wire_rg_) reserve_pat(g->pat);
+  for (const Group* g : wire_lg_) reserve_pat(g->pat);
 
   int32_t* dbase = nullptr;
   if (blob_n) {
@@ -469,16 +539,16 @@ DevPlan& StarForest::dev() {
     d->self_root_distinct = leaf_groups_.front().pat.distinct;
   }
   int64_t off = 0;
-  for (size_t gi = self ? 1 : 0; gi < root_groups_.size(); ++gi) {
-    const auto& g = root_groups_[gi];
+  for (const Group* gp : wire_rg_) {
+    const auto& g = *gp;
     const int64_t cnt = g.count();
     d->rg.push_back({g.rank, cnt, off, dpat(g.pat), g.pat.is_contiguous(), g.pat.start, g.pat.distinct});
     off += cnt;
   }
   d->n_leafside = off;
   off = 0;
-  for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size(); ++gi) {
-    const auto& g = leaf_groups_[gi];
+  for (const Group* gp : wire_lg_) {
+    const auto& g = *gp;
     const int64_t cnt = g.count();
     d->lg.push_back({g.rank, cnt, off, dpat(g.pat), g.pat.is_contiguous(), g.pat.start, g.pat.distinct});
     off += cnt;
@@ -532,9 +602,7 @@ void StarForest::ensure_csr() {
   };
   std::vector<Part> parts;
   if (self) parts.push_back({&leaf_groups_.front(), &root_groups_.front(), 0});
-  size_t k = 0;
-  for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size(); ++gi, ++k)
-    parts.push_back({&leaf_groups_[gi], nullptr, d.lg[k].stage_off});
+  for (size_t k = 0; k < wire_lg_.size(); ++k) parts.push_back({wire_lg_[k], nullptr, d.lg[k].stage_off});
   int64_t total = 0;
   for (const auto& q : parts) total += q.lg->count();
   SFG_REQUIRE(total <= kI32Max, "CSR exceeds the int32 range of device plans");
@@ -548,7 +616,7 @@ void StarForest::ensure_csr() {
   int64_t at = 0;
   for (const auto& q : parts) {
     const int64_t m = q.lg->count();
-    if (on_device) {
+    if (on_device) {  // (re-sorted groups exist only once host copies were made)
       const int64_t* vals =
           q.rg ? dg_->ridx + (q.rg->ditems - dg_->ords) : nullptr;  // leaf indices of the self edges
       dev_csr_fill(q.lg->ditems, vals, m, q.base, key + at, val + at);
@@ -598,8 +666,8 @@ void StarForest::ensure_csr_host() {
       ++cnt_self[static_cast<size_t>(r)];
       ++cnt_all[static_cast<size_t>(r)];
     }
-  for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size(); ++gi)
-    for (int64_t r : leaf_groups_[gi].items) ++cnt_all[static_cast<size_t>(r)];
+  for (const Group* g : wire_lg_)
+    for (int64_t r : g->items) ++cnt_all[static_cast<size_t>(r)];
 
   std::vector<int32_t> roots, offs, split;
   std::vector<int64_t> cursor(static_cast<size_t>(nroots_), -1);
@@ -625,9 +693,8 @@ void StarForest::ensure_csr_host() {
       ent[static_cast<size_t>(cursor[static_cast<size_t>(lg.items[i])]++)] = static_cast<int32_t>(leaf);
     }
   }
-  size_t k = 0;
-  for (size_t gi = self ? 1 : 0; gi < leaf_groups_.size(); ++gi, ++k) {
-    const auto& g = leaf_groups_[gi];
+  for (size_t k = 0; k < wire_lg_.size(); ++k) {
+    const auto& g = *wire_lg_[k];
     const int64_t base = d.lg[k].stage_off;
     for (size_t i = 0; i < g.items.size(); ++i)
       ent[static_cast<size_t>(cursor[static_cast<size_t>(g.items[i])]++)] =
