@@ -155,10 +155,10 @@ DSeg csr_seg(const DevPlan& d, CsrRange range, int32_t type, bool seq, size_t ub
   // advances 32 roots) whenever there are enough roots to spread over the
   // GPU; a warp per root only for few, very high-degree roots.
   // Order-free fetch-and-op (integer ops, free-order mode) keeps a warp per
-  // root (warp scan, exact for them) up to 32768 roots: the fetch's thread
+  // root (warp scan, exact for them) below 65,536 roots: the fetch's thread
   // chains are the slower ones, and with that few roots they leave the GPU
   // mostly idle (config 4 at N=4: fetch End 170 -> 100 us; the same rule for
-  // folds made Begin's local fold 8 -> 58 us, so folds stay thread per root).
+  // Begin's local fold made it 8 -> 58 us, so that fold stays thread per root).
   static const int64_t warp_limit = [] {
     const char* e = std::getenv("SFG_CSR_WARP_LIMIT");
     return e ? std::atoll(e) : int64_t(32768);
@@ -167,8 +167,12 @@ DSeg csr_seg(const DevPlan& d, CsrRange range, int32_t type, bool seq, size_t ub
   // through shuffles: config 4 at N=4 (16,384 roots per rank) FetchAndOp f64
   // 309 -> 256 us (profiles/r2_cfg4_n4*.log); SFG_CSR_NO_WARP_SEQ restores
   // thread per root for them.
+  // The fetch's limit is twice the fold's: at 32,768 roots (config 4 at N=2)
+  // the warp form still wins for the fetch (End 425 -> 398 us f64, 428 ->
+  // 345 us i64) but loses for the fold (Reduce i64 170 -> 197 us); at 65,536
+  // (N=1) thread per root wins for both (fetch 223 vs 460 us).
   static const bool no_warp_seq = std::getenv("SFG_CSR_NO_WARP_SEQ") != nullptr;
-  const bool warp_fetch = type == SEG_CSR_FETCH && (!seq || !no_warp_seq) && s.n < warp_limit;
+  const bool warp_fetch = type == SEG_CSR_FETCH && (!seq || !no_warp_seq) && s.n < 2 * warp_limit;
   // End's order-free folds (integers, free-order floats) over the roots that
   // receive remote contributions (every root of a rank in config 4 at N>1,
   // ~256 contributions each) likewise: config 4 Reduce at N=4 143 -> 125 us.

@@ -194,3 +194,40 @@ def test_first_operation_captured_in_a_cuda_graph():
     assert np.array_equal(second[0], want_r2[0]) and np.array_equal(second[1], want_u2[0])
     assert "prepare" in msg, msg
     assert np.array_equal(r3got, want3[0])
+
+
+@pytest.mark.parametrize("device_graph", [False, True])
+def test_message_order_is_invisible(device_graph):
+    """Remote groups travel sorted by root offset (StarForest::build_wire_order;
+    every group of a random forest is re-sorted): deterministic float64
+    FetchAndOp SUM and Reduce SUM — the order-sensitive cases — still equal
+    the oracle bit for bit, for host- and device-set graphs, and the group
+    plans the API exports keep the reference's order after the device plan
+    was built."""
+    specs = graphs.random_graph_specs(77, 4, 400)
+    roots = rank_data(specs, 3, np.float64, 1, 100, "root")
+    leaves = rank_data(specs, 3, np.float64, 1, 200, "leaf")
+    upd = [np.zeros_like(x) for x in leaves]
+    got = run_gpu(specs, "fetch_and_op", [roots, leaves, upd], op="sum", device_graph=device_graph)
+    want_r, want_u = O.fetch_and_op(specs, roots, leaves, upd, "sum")
+    assert_same(got[0], want_r, what="fetch roots")
+    assert_same(got[2], want_u, what="fetch leafupdate")
+    got = run_gpu(specs, "reduce", [leaves, roots], op="sum", device_graph=device_graph)
+    assert_same(got[1], O.reduce(specs, leaves, roots, "sum"), what="reduce")
+
+    import torch
+
+    def body(comm):
+        f = sf.StarForest(comm)
+        f.set_graph_spec(specs[comm.rank()])
+        f.setup()
+        before = [(g.rank, g.items.copy()) for g in f.root_groups() + f.leaf_groups()]
+        leaf = to_dev(leaves[comm.rank()])
+        root = to_dev(roots[comm.rank()])
+        sf.reduce_end(sf.reduce_begin(f, sf.Unit(sf.Kind.float64), leaf, root, sf.ReduceOp.sum, None))
+        torch.cuda.synchronize()
+        after = [(g.rank, g.items.copy()) for g in f.root_groups() + f.leaf_groups()]
+        return len(before) == len(after) and all(
+            a[0] == b[0] and np.array_equal(a[1], b[1]) for a, b in zip(before, after))
+
+    assert all(sf.run_ranks(sf.CommConfig(nranks=len(specs)), body))
