@@ -508,11 +508,17 @@ def config3_spmv(ctx, args):
     # the eager period at N>1 where the ranks' exchanges couple them.
     ms_o = timed_graph(ctx, overlapped, 20, 3)
     ms_s = timed_graph(ctx, serial, 20, 3)
+
+    def transpose():  # spmv.hpp:161-169: y = A^T x; lvec = B^T x; Reduce SUM lvec -> y
+        S.spmv_transpose(f, D, B, x, lvec, y, ctx.stream)
+
+    ms_t = timed_graph(ctx, transpose, 20, 3)
     kern = {k: 1e3 * v["total_ms"] / v["launches"] for k, v in rec.items()}
     emit(ctx, {"config": 3, "op": "spmv_27pt", "n_gpus": ctx.world, "grid": [N] * 3,
                "dims": list(dims), "rows": layout.total(), "nnz": nnz,
                "us_per_spmv": ms_o * 1e3, "us_exchange_then_spmv": ms_s * 1e3,
                "us_per_spmv_eager": e_o * 1e3, "us_exchange_then_spmv_eager": e_s * 1e3,
+               "us_per_spmv_transpose": ms_t * 1e3,
                "GFLOPs": 2 * nnz / (ms_o * 1e-3) / 1e9,
                "GBps_algorithmic": byts / (ms_o * 1e-3) / 1e9,
                "frac_hbm_per_gpu": byts / ctx.world / (ms_o * 1e-3) / 1e9 / peak(),
