@@ -333,14 +333,23 @@ def config2(ctx, args):
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
         sf._lib().sfg_trace_dump(os.path.join(ROOT, "gpurun_out", f"trace_cfg2_r{ctx.rank}.jsonl").encode())
         del g
-    for name, fn in (("bcast_replace", bc), ("reduce_sum", rd)):
+    def bc1():  # one-shot forms (ops.hpp:60, 68): no caller work between the halves
+        sf.bcast(f, u, root, leaf, sf.ReduceOp.replace, ctx.stream, sync=False)
+
+    def rd1():
+        sf.reduce(f, u, leaf, root, sf.ReduceOp.sum, ctx.stream, sync=False)
+
+    for name, fn, fn1 in (("bcast_replace", bc, bc1), ("reduce_sum", rd, rd1)):
         ms, byts, rec = ctx.timed(fn, args.steps, args.warmup, flush=False)
         gms = timed_graph(ctx, fn, args.steps, args.warmup)
+        gms1 = timed_graph(ctx, fn1, args.steps, args.warmup)
         nbytes = ctx.vmax(float(sum(v.get("link_bytes", 0) for v in rec.values()) / args.steps))
         op_line(ctx, 2, name, ms, byts, rec, {"variant": "halo-only", "grid": [N] * 3,
                                                "nleaves_rank0": int(spec.nleaves), "setup_s": setup_s,
                                                "graph_us_per_op": gms * 1e3,
-                                               "graph_link_GBps_max_rank_egress": nbytes / (gms * 1e-3) / 1e9})
+                                               "graph_link_GBps_max_rank_egress": nbytes / (gms * 1e-3) / 1e9,
+                                               "graph_us_per_op_one_shot": gms1 * 1e3,
+                                               "graph_link_GBps_one_shot": nbytes / (gms1 * 1e-3) / 1e9})
 
 
 # ------------------------------------------------------------------ config 4
@@ -411,10 +420,9 @@ def config5(ctx, args):
             t0 = time.perf_counter()
             with torch.cuda.stream(ctx.stream):
                 e0.record(ctx.stream)
-                h = sf.bcast_begin(f, u, root, leaf, sf.ReduceOp.replace, ctx.stream)
-                sf.bcast_end(h)
-                h = sf.reduce_begin(f, u, leaf, root, sf.ReduceOp.replace, ctx.stream)
-                sf.reduce_end(h)
+                # the one-shot forms, as the reference's ping-pong (bench.cpp:65-66)
+                sf.bcast(f, u, root, leaf, sf.ReduceOp.replace, ctx.stream, sync=False)
+                sf.reduce(f, u, leaf, root, sf.ReduceOp.replace, ctx.stream, sync=False)
                 e1.record(ctx.stream)
             ctx.stream.synchronize()
             t1 = time.perf_counter()
@@ -426,12 +434,18 @@ def config5(ctx, args):
             ok = bool((leaf.cpu() == torch.arange(n)).all()) if n else True
 
         def rt():
+            sf.bcast(f, u, root, leaf, sf.ReduceOp.replace, ctx.stream, sync=False)
+            sf.reduce(f, u, leaf, root, sf.ReduceOp.replace, ctx.stream, sync=False)
+
+        def rt_split():  # split-phase Begin/End (exchange on a forked stream)
             h = sf.bcast_begin(f, u, root, leaf, sf.ReduceOp.replace, ctx.stream)
             sf.bcast_end(h)
             h = sf.reduce_begin(f, u, leaf, root, sf.ReduceOp.replace, ctx.stream)
             sf.reduce_end(h)
 
-        graph_half = timed_graph(ctx, rt, 20 if size <= (1 << 22) else 4, 2) * 1e3 / 2
+        reps = 20 if size <= (1 << 22) else 4
+        graph_half = timed_graph(ctx, rt, reps, 2) * 1e3 / 2
+        graph_half_split = timed_graph(ctx, rt_split, reps, 2) * 1e3 / 2
         if ctx.rank == 1:
             ok = ok and (bool((leaf.cpu() == torch.arange(n)).all()) if n else True)
         dmed = ctx.vmax(statistics.median(dev_us))
@@ -440,6 +454,7 @@ def config5(ctx, args):
         rows.append({"bytes": size, "half_rtt_us_median": dmed, "half_rtt_us_min": dmin,
                      "host_half_rtt_us_median": hmed, "GBps": size / (dmed * 1e-6) / 1e9,
                      "graph_half_rtt_us": graph_half, "graph_GBps": size / (graph_half * 1e-6) / 1e9,
+                     "graph_half_rtt_us_split_phase": graph_half_split,
                      "payload_ok": ok})
         del f
         size *= 2

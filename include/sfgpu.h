@@ -187,6 +187,21 @@ int sfg_gather_end(sfg_handle h);
 int sfg_scatter_begin(sfg_sf sf, int kind, int64_t blocklen, const void* multirootdata,
                       void* leafdata, void* stream, sfg_handle* out);
 int sfg_scatter_end(sfg_handle h);
+/* One-shot operations (ops.hpp:60, 68, 79, 88, 94: bcast, reduce,
+   fetch_and_op, gather, scatter), stream-ordered: Begin and End back to back
+   on `stream` (synchronise it to get the reference's blocking behaviour).
+   With nothing of the caller's between the halves, the p2p exchange runs on
+   `stream` itself instead of a forked communicator stream. */
+int sfg_bcast(sfg_sf sf, int kind, int64_t blocklen, const void* rootdata, void* leafdata, int op,
+              void* stream);
+int sfg_reduce(sfg_sf sf, int kind, int64_t blocklen, const void* leafdata, void* rootdata, int op,
+               void* stream);
+int sfg_fetch_and_op(sfg_sf sf, int kind, int64_t blocklen, void* rootdata, const void* leafdata,
+                     void* leafupdate, int op, void* stream);
+int sfg_gather(sfg_sf sf, int kind, int64_t blocklen, const void* leafdata, void* multirootdata,
+               void* stream);
+int sfg_scatter(sfg_sf sf, int kind, int64_t blocklen, const void* multirootdata, void* leafdata,
+                void* stream);
 /* Graph algebra (starforest.hpp:150-171). Collective over the operands'
  * communicator; the new forest is set up (identity: graph set, as the
  * reference's identity_sf). compose: roots of A, leaves of B, an edge where an

@@ -62,6 +62,10 @@ inline void check(int rc) {
   if (rc == SFG_ERR_TIMEOUT) throw TimeoutError(msg);
   throw Error(msg);
 }
+// The one-shot forms block like the reference's (ops.cpp: Begin + End).
+inline void sync(cudaStream_t s) {
+  if (cudaStreamSynchronize(s) != cudaSuccess) throw Error("stream synchronisation failed");
+}
 }  // namespace detail
 
 struct RootRef {
@@ -327,9 +331,9 @@ inline OpHandle bcast_begin(StarForest& sf, const Unit& u, const void* rootdata,
 inline void bcast_end(OpHandle& h) { detail::check(sfg_bcast_end(h.handle())); }
 inline void bcast(StarForest& sf, const Unit& u, const void* rootdata, void* leafdata, ReduceOp op,
                   cudaStream_t s = nullptr) {
-  OpHandle h = bcast_begin(sf, u, rootdata, leafdata, op, s);
-  bcast_end(h);
-  h.wait();
+  detail::check(sfg_bcast(sf.handle(), static_cast<int>(u.kind), u.blocklen, rootdata, leafdata,
+                          static_cast<int>(op), s));
+  detail::sync(s);
 }
 
 inline OpHandle reduce_begin(StarForest& sf, const Unit& u, const void* leafdata, void* rootdata,
@@ -342,9 +346,9 @@ inline OpHandle reduce_begin(StarForest& sf, const Unit& u, const void* leafdata
 inline void reduce_end(OpHandle& h) { detail::check(sfg_reduce_end(h.handle())); }
 inline void reduce(StarForest& sf, const Unit& u, const void* leafdata, void* rootdata, ReduceOp op,
                    cudaStream_t s = nullptr) {
-  OpHandle h = reduce_begin(sf, u, leafdata, rootdata, op, s);
-  reduce_end(h);
-  h.wait();
+  detail::check(sfg_reduce(sf.handle(), static_cast<int>(u.kind), u.blocklen, leafdata, rootdata,
+                           static_cast<int>(op), s));
+  detail::sync(s);
 }
 
 inline OpHandle fetch_and_op_begin(StarForest& sf, const Unit& u, void* rootdata,
@@ -358,9 +362,9 @@ inline OpHandle fetch_and_op_begin(StarForest& sf, const Unit& u, void* rootdata
 inline void fetch_and_op_end(OpHandle& h) { detail::check(sfg_fetch_and_op_end(h.handle())); }
 inline void fetch_and_op(StarForest& sf, const Unit& u, void* rootdata, const void* leafdata,
                          void* leafupdate, ReduceOp op, cudaStream_t s = nullptr) {
-  OpHandle h = fetch_and_op_begin(sf, u, rootdata, leafdata, leafupdate, op, s);
-  fetch_and_op_end(h);
-  h.wait();
+  detail::check(sfg_fetch_and_op(sf.handle(), static_cast<int>(u.kind), u.blocklen, rootdata, leafdata,
+                                 leafupdate, static_cast<int>(op), s));
+  detail::sync(s);
 }
 
 inline OpHandle gather_begin(StarForest& sf, const Unit& u, const void* leafdata,
@@ -373,9 +377,8 @@ inline OpHandle gather_begin(StarForest& sf, const Unit& u, const void* leafdata
 inline void gather_end(OpHandle& h) { detail::check(sfg_gather_end(h.handle())); }
 inline void gather(StarForest& sf, const Unit& u, const void* leafdata, void* multirootdata,
                    cudaStream_t s = nullptr) {
-  OpHandle h = gather_begin(sf, u, leafdata, multirootdata, s);
-  gather_end(h);
-  h.wait();
+  detail::check(sfg_gather(sf.handle(), static_cast<int>(u.kind), u.blocklen, leafdata, multirootdata, s));
+  detail::sync(s);
 }
 
 inline OpHandle scatter_begin(StarForest& sf, const Unit& u, const void* multirootdata,
@@ -388,9 +391,8 @@ inline OpHandle scatter_begin(StarForest& sf, const Unit& u, const void* multiro
 inline void scatter_end(OpHandle& h) { detail::check(sfg_scatter_end(h.handle())); }
 inline void scatter(StarForest& sf, const Unit& u, const void* multirootdata, void* leafdata,
                     cudaStream_t s = nullptr) {
-  OpHandle h = scatter_begin(sf, u, multirootdata, leafdata, s);
-  scatter_end(h);
-  h.wait();
+  detail::check(sfg_scatter(sf.handle(), static_cast<int>(u.kind), u.blocklen, multirootdata, leafdata, s));
+  detail::sync(s);
 }
 
 // ------------------------------------------------------------ harness

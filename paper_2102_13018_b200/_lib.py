@@ -103,6 +103,11 @@ _SIGS = {
     "sfg_sf_compute_degrees": (C.c_int, [_V, _V]),
     "sfg_sf_multi_sf": (C.c_int, [_V, C.POINTER(_V)]),
     "sfg_sf_graph": (C.c_int, [_V, _V, _V, _V]),
+    "sfg_bcast": (C.c_int, [_V, C.c_int, C.c_int64, _V, _V, C.c_int, _V]),
+    "sfg_reduce": (C.c_int, [_V, C.c_int, C.c_int64, _V, _V, C.c_int, _V]),
+    "sfg_fetch_and_op": (C.c_int, [_V, C.c_int, C.c_int64, _V, _V, _V, C.c_int, _V]),
+    "sfg_gather": (C.c_int, [_V, C.c_int, C.c_int64, _V, _V, _V]),
+    "sfg_scatter": (C.c_int, [_V, C.c_int, C.c_int64, _V, _V, _V]),
     "sfg_bcast_begin": (C.c_int, [_V, C.c_int, C.c_int64, _V, _V, C.c_int, _V, C.POINTER(_V)]),
     "sfg_bcast_end": (C.c_int, [_V]),
     "sfg_reduce_begin": (C.c_int, [_V, C.c_int, C.c_int64, _V, _V, C.c_int, _V, C.POINTER(_V)]),

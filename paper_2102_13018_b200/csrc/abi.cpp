@@ -372,6 +372,29 @@ int sfg_bcast_end(sfg_handle h) {
   return guard([&] { sfg::bcast_end(*H(h)); });
 }
 
+int sfg_bcast(sfg_sf sf, int kind, int64_t blocklen, const void* rootdata, void* leafdata, int op,
+              void* stream) {
+  return guard([&] { sfg::bcast(*SF(sf), unit(kind, blocklen), rootdata, leafdata, rop(op), st(stream)); });
+}
+int sfg_reduce(sfg_sf sf, int kind, int64_t blocklen, const void* leafdata, void* rootdata, int op,
+               void* stream) {
+  return guard([&] { sfg::reduce(*SF(sf), unit(kind, blocklen), leafdata, rootdata, rop(op), st(stream)); });
+}
+int sfg_fetch_and_op(sfg_sf sf, int kind, int64_t blocklen, void* rootdata, const void* leafdata,
+                     void* leafupdate, int op, void* stream) {
+  return guard([&] {
+    sfg::fetch_and_op(*SF(sf), unit(kind, blocklen), rootdata, leafdata, leafupdate, rop(op), st(stream));
+  });
+}
+int sfg_gather(sfg_sf sf, int kind, int64_t blocklen, const void* leafdata, void* multirootdata,
+               void* stream) {
+  return guard([&] { sfg::gather(*SF(sf), unit(kind, blocklen), leafdata, multirootdata, st(stream)); });
+}
+int sfg_scatter(sfg_sf sf, int kind, int64_t blocklen, const void* multirootdata, void* leafdata,
+                void* stream) {
+  return guard([&] { sfg::scatter(*SF(sf), unit(kind, blocklen), multirootdata, leafdata, st(stream)); });
+}
+
 int sfg_reduce_begin(sfg_sf sf, int kind, int64_t blocklen, const void* leafdata, void* rootdata,
                      int op, void* stream, sfg_handle* out) {
   return guard([&] {

@@ -567,6 +567,7 @@ struct OpHandle {
   bool forked = false;              // p2p: the puts ran on the comm stream
   bool fused_unpack = false;        // p2p Bcast: the unpack ran in the put launch
   bool ll_direct = false;           // p2p Reduce: remote contributions applied in the put launch
+  bool immediate = false;           // one-shot form: End follows Begin with nothing in between
   bool coupled_split = false;       // reduce: coupled roots folded in End (DevPlan::coupled_bits)
   std::vector<uint8_t> zero_copy_recv;
   std::vector<int32_t> fetch_order;  // free-order fetch: group order used (empty: stored order)
@@ -594,6 +595,13 @@ void gather_end(OpHandle& h);
 std::unique_ptr<OpHandle> scatter_begin(StarForest& sf, const Unit& u, const void* multirootdata,
                                         void* leafdata, cudaStream_t s);
 void scatter_end(OpHandle& h);
+// One-shot forms (ops.hpp:60-94), stream-ordered: Begin and End back to back.
+void bcast(StarForest& sf, const Unit& u, const void* rootdata, void* leafdata, ReduceOp op, cudaStream_t s);
+void reduce(StarForest& sf, const Unit& u, const void* leafdata, void* rootdata, ReduceOp op, cudaStream_t s);
+void fetch_and_op(StarForest& sf, const Unit& u, void* rootdata, const void* leafdata, void* leafupdate,
+                  ReduceOp op, cudaStream_t s);
+void gather(StarForest& sf, const Unit& u, const void* leafdata, void* multirootdata, cudaStream_t s);
+void scatter(StarForest& sf, const Unit& u, const void* multirootdata, void* leafdata, cudaStream_t s);
 
 DPat to_dpat(const Pattern& p, const int32_t* dev_idx);
 

@@ -636,40 +636,42 @@ def scatter_end(h: OpHandle) -> None:
     _check(_lib().sfg_scatter_end(h._h))
 
 
-def _sync(h: OpHandle) -> None:
-    import torch
+def _one_shot(fn, args: list, stream, sync: bool) -> None:
+    s = _stream(stream)
+    _check(fn(*args, s))
+    if sync:
+        import torch
 
-    torch.cuda.ExternalStream(h.stream).synchronize() if h.stream else torch.cuda.synchronize()
-
-
-def bcast(sf, unit, rootdata, leafdata, op, stream=None) -> None:
-    h = bcast_begin(sf, unit, rootdata, leafdata, op, stream)
-    bcast_end(h)
-    _sync(h)
+        torch.cuda.ExternalStream(s).synchronize()
 
 
-def reduce(sf, unit, leafdata, rootdata, op, stream=None) -> None:
-    h = reduce_begin(sf, unit, leafdata, rootdata, op, stream)
-    reduce_end(h)
-    _sync(h)
+# One-shot forms (ops.hpp:60, 68, 79, 88, 94): Begin + End back to back on
+# `stream`. sync=True blocks like the reference's; sync=False leaves them
+# stream-ordered (CUDA-graph capturable). With nothing of the caller's between
+# the halves, the p2p exchange runs on the stream itself (no fork / join).
+def bcast(sf, unit, rootdata, leafdata, op, stream=None, sync: bool = True) -> None:
+    _one_shot(_lib().sfg_bcast, [sf._h, int(unit.kind), unit.blocklen, _ptr(rootdata), _ptr(leafdata),
+                                 int(op)], stream, sync)
 
 
-def fetch_and_op(sf, unit, rootdata, leafdata, leafupdate, op, stream=None) -> None:
-    h = fetch_and_op_begin(sf, unit, rootdata, leafdata, leafupdate, op, stream)
-    fetch_and_op_end(h)
-    _sync(h)
+def reduce(sf, unit, leafdata, rootdata, op, stream=None, sync: bool = True) -> None:
+    _one_shot(_lib().sfg_reduce, [sf._h, int(unit.kind), unit.blocklen, _ptr(leafdata), _ptr(rootdata),
+                                  int(op)], stream, sync)
 
 
-def gather(sf, unit, leafdata, multirootdata, stream=None) -> None:
-    h = gather_begin(sf, unit, leafdata, multirootdata, stream)
-    gather_end(h)
-    _sync(h)
+def fetch_and_op(sf, unit, rootdata, leafdata, leafupdate, op, stream=None, sync: bool = True) -> None:
+    _one_shot(_lib().sfg_fetch_and_op, [sf._h, int(unit.kind), unit.blocklen, _ptr(rootdata), _ptr(leafdata),
+                                        _ptr(leafupdate), int(op)], stream, sync)
 
 
-def scatter(sf, unit, multirootdata, leafdata, stream=None) -> None:
-    h = scatter_begin(sf, unit, multirootdata, leafdata, stream)
-    scatter_end(h)
-    _sync(h)
+def gather(sf, unit, leafdata, multirootdata, stream=None, sync: bool = True) -> None:
+    _one_shot(_lib().sfg_gather, [sf._h, int(unit.kind), unit.blocklen, _ptr(leafdata), _ptr(multirootdata)],
+              stream, sync)
+
+
+def scatter(sf, unit, multirootdata, leafdata, stream=None, sync: bool = True) -> None:
+    _one_shot(_lib().sfg_scatter, [sf._h, int(unit.kind), unit.blocklen, _ptr(multirootdata), _ptr(leafdata)],
+              stream, sync)
 
 
 # --------------------------------------------------------------- counters
