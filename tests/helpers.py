@@ -33,7 +33,7 @@ def to_host(t) -> np.ndarray:
 def run_gpu(specs, opkind: str, data: list[list[np.ndarray]], op: str = "replace",
             blocklen: int = 1, config: sf.CommConfig | None = None, devices=None,
             setup_alg=sf.SetupAlg.automatic, two_phase: bool = False,
-            device_graph: bool = False):
+            device_graph: bool = False, one_shot: bool = False):
     """data: per-buffer list of per-rank arrays, in the op's argument order:
     bcast (root, leaf) reduce (leaf, root) fetch_and_op (root, leaf, update)
     gather (leaf, multiroot) scatter (multiroot, leaf). Returns the same
@@ -58,7 +58,15 @@ def run_gpu(specs, opkind: str, data: list[list[np.ndarray]], op: str = "replace
         bufs = [to_dev(d[r]) for d in data]
         stream = torch.cuda.Stream()
         with torch.cuda.stream(stream):
-            if opkind == "bcast":
+            if one_shot:  # sfg_bcast & co: Begin + End back to back (no p2p stream fork)
+                one = {"bcast": lambda: sf.bcast(f, unit, bufs[0], bufs[1], rop, stream, sync=False),
+                       "reduce": lambda: sf.reduce(f, unit, bufs[0], bufs[1], rop, stream, sync=False),
+                       "fetch_and_op": lambda: sf.fetch_and_op(f, unit, bufs[0], bufs[1], bufs[2], rop, stream,
+                                                               sync=False),
+                       "gather": lambda: sf.gather(f, unit, bufs[0], bufs[1], stream, sync=False),
+                       "scatter": lambda: sf.scatter(f, unit, bufs[0], bufs[1], stream, sync=False)}
+                one[opkind]()
+            elif opkind == "bcast":
                 h = sf.bcast_begin(f, unit, bufs[0], bufs[1], rop, stream)
                 sf.bcast_end(h)
             elif opkind == "reduce":

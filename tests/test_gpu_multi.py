@@ -1,6 +1,7 @@
 """Multi-GPU parity: ranks on distinct B200s, NCCL data plane (threads of one
 process, and one process per GPU via torch.distributed.run), and the
 in-process transport's peer copies across devices. Skipped below 2 GPUs."""
+import functools
 import os
 import subprocess
 import sys
@@ -11,6 +12,7 @@ import pytest
 from oracle import oracle as O
 from paper_2102_13018_b200 import graphs, sf
 from tests.helpers import assert_same, rank_data, run_gpu
+from tests.helpers import run_gpu as _run_gpu
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -327,13 +329,16 @@ def test_p2p_puts_never_stage_on_the_sender():
 
 
 @need2
+@pytest.mark.parametrize("one_shot", [False, True])
 @pytest.mark.parametrize("dtype,bl", [(np.int32, 2), (np.int32, 3), (np.int32, 4), (np.uint8, 16), (np.uint8, 5)])
-def test_p2p_protocol_per_unit_size(dtype, bl):
+def test_p2p_protocol_per_unit_size(dtype, bl, one_shot):
     """The p2p slot protocol follows the unit size: whole 8-byte words ->
     LL128 lines (int32 x 2 / x 4: two elements per word; 16 opaque bytes),
     other sizes -> the flag protocol (int32 x 3, 5 opaque bytes). Both
-    bit-exact against the oracle between GPUs."""
+    bit-exact against the oracle between GPUs, split-phase and through the
+    one-shot forms (exchange on the caller's stream, no fork)."""
     n = min(ngpu(), 4)
+    run_gpu = functools.partial(_run_gpu, one_shot=one_shot)
     specs = graphs.random_graph_specs(61, n, 60)
     roots = rank_data(specs, 4, dtype, bl, 100, "root")
     leaves = rank_data(specs, 4, dtype, bl, 200, "leaf")
