@@ -21,6 +21,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <type_traits>
+#include <utility>
 
 #include "kernels.hpp"
 
@@ -862,6 +863,18 @@ __device__ __forceinline__ void count_put_ll(const DSeg& seg, int64_t nblk) {
   }
 }
 
+// Programmatic dependent launch: every library kernel is launched with
+// programmatic stream serialization and starts by (1) allowing its own
+// dependent launch to be scheduled (all of this grid's CTAs have then started,
+// so the dependent's waiting CTAs never take a slot this grid still needs) and
+// (2) waiting until the previous kernel on the stream has completed and its
+// memory is visible — the same guarantee as a plain kernel boundary, with the
+// launch latency of back-to-back exchanges overlapped.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // FULL = the launch contains root-sorted (CSR) or fetch segments. Pair-only
 // launches (every pack, unpack and structured local scatter) get their own
 // instantiation so the CSR paths do not raise their register allocation.
@@ -871,6 +884,7 @@ __device__ __forceinline__ void count_put_ll(const DSeg& seg, int64_t nblk) {
 template <class T, int OP, int MODE>
 __global__ void __launch_bounds__(kThreads, MODE == 0 ? 4 : MODE == 1 ? 3 : 2)
     segments_kernel(const __grid_constant__ LaunchParams P) {
+  pdl_enter();
   constexpr bool FULL = MODE == 1;
   int64_t b = blockIdx.x;
   if (P.ilv_a > 0) {  // interleave group A (puts, local) with group B (receives)
@@ -964,6 +978,7 @@ __global__ void __launch_bounds__(kThreads, MODE == 0 ? 4 : MODE == 1 ? 3 : 2)
 // of the per-root chains.
 template <class T, int OP, bool FETCH>
 __global__ void __launch_bounds__(kThreads, 4) csr_kernel(const __grid_constant__ LaunchParams P) {
+  pdl_enter();
   const DSeg& seg = P.seg[0];
   if (seg.wait_mask) wait_flags(P, seg.wait_mask);
   if constexpr (OP != OP_REPLACE) run_csr_t<T, OP, 8, FETCH, LaunchParams>(seg, P, blockIdx.x);
@@ -984,6 +999,7 @@ struct SoloParams {
 
 template <class T, int OP>
 __global__ void __launch_bounds__(kThreads, 4) pair_solo(const __grid_constant__ SoloParams P) {
+  pdl_enter();
   if (P.seg.run > 0)
     run_pair_rows<T, OP, SoloParams>(P.seg, P, blockIdx.x);
   else
@@ -992,6 +1008,7 @@ __global__ void __launch_bounds__(kThreads, 4) pair_solo(const __grid_constant__
 
 template <class T, int OP, bool FETCH>
 __global__ void __launch_bounds__(kThreads, 4) csr_solo(const __grid_constant__ SoloParams P) {
+  pdl_enter();
   if constexpr (OP != OP_REPLACE) run_csr_t<T, OP, 8, FETCH, SoloParams>(P.seg, P, blockIdx.x);
 }
 
@@ -1013,6 +1030,30 @@ SoloParams solo_of(const LaunchParams& p) {
   return q;
 }
 
+// Launch, with programmatic stream serialization when `pdl` (see pdl_enter):
+// the exchange launches (LL128 put/receive) and the signalling kernel, whose
+// back-to-back launches are latency-bound; local bulk work launches plainly
+// (PDL there measured -2 % on the N=2 headline step). SFG_NO_PDL=1 turns it
+// off (ablation). Errors surface through cudaGetLastError like <<<>>>.
+bool pdl_on() {
+  static const bool on = std::getenv("SFG_NO_PDL") == nullptr;
+  return on;
+}
+template <class... K, class... A>
+void launch_k(void (*kernel)(K...), int64_t blocks, int threads, cudaStream_t st, bool pdl, A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+  cfg.blockDim = dim3(static_cast<unsigned>(threads));
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl && pdl_on() ? 1 : 0;
+  (void)cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
+}
+
 template <class T, int OP>
 void launch_t(const LaunchParams& p, int64_t blocks, cudaStream_t st) {
   bool full = false;  // CSR / fetch segments present
@@ -1023,38 +1064,38 @@ void launch_t(const LaunchParams& p, int64_t blocks, cudaStream_t st) {
     const SoloParams q = solo_of(p);
     if (p.seg[0].type == SEG_PAIR) {
       if (p.seg[0].replace)
-        pair_solo<T, OP_REPLACE><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(q);
+        launch_k(pair_solo<T, OP_REPLACE>, blocks, kThreads, st, false, q);
       else
-        pair_solo<T, OP><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(q);
+        launch_k(pair_solo<T, OP>, blocks, kThreads, st, false, q);
       return;
     }
     if constexpr (OP != OP_REPLACE && (std::is_same_v<T, double> || std::is_same_v<T, int64_t> ||
                                        std::is_same_v<T, int32_t>)) {
       if (p.seg[0].type == SEG_CSR_FETCH)
-        csr_solo<T, OP, true><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(q);
+        launch_k(csr_solo<T, OP, true>, blocks, kThreads, st, false, q);
       else
-        csr_solo<T, OP, false><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(q);
+        launch_k(csr_solo<T, OP, false>, blocks, kThreads, st, false, q);
       return;
     }
   }
   bool ll = false;
   for (int s = 0; s < p.nseg; ++s) ll = ll || p.seg[s].type == SEG_PUT_LL || p.seg[s].type == SEG_RECV_LL;
   if (ll && !full) {
-    segments_kernel<T, OP, 2><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
+    launch_k(segments_kernel<T, OP, 2>, blocks, kThreads, st, true, p);
   } else if constexpr (OP == OP_REPLACE) {
-    segments_kernel<T, OP, 0><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
+    launch_k(segments_kernel<T, OP, 0>, blocks, kThreads, st, false, p);
   } else if (p.nseg == 1 && (p.seg[0].type == SEG_CSR_FOLD || p.seg[0].type == SEG_CSR_FETCH) &&
              !p.seg[0].csr_warp && (std::is_same_v<T, double> || std::is_same_v<T, int64_t> ||
                                     std::is_same_v<T, int32_t>)) {
     if (p.seg[0].type == SEG_CSR_FETCH)
-      csr_kernel<T, OP, true><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
+      launch_k(csr_kernel<T, OP, true>, blocks, kThreads, st, false, p);
     else
-      csr_kernel<T, OP, false><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
+      launch_k(csr_kernel<T, OP, false>, blocks, kThreads, st, false, p);
   } else {
     if (full)
-      segments_kernel<T, OP, 1><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
+      launch_k(segments_kernel<T, OP, 1>, blocks, kThreads, st, false, p);
     else
-      segments_kernel<T, OP, 0><<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(p);
+      launch_k(segments_kernel<T, OP, 0>, blocks, kThreads, st, false, p);
   }
 }
 
@@ -1241,6 +1282,7 @@ __global__ void quiesce_kernel(const __grid_constant__ FlagBatch q, unsigned lon
 }
 
 __global__ void signal_kernel(const __grid_constant__ FlagBatch q) {
+  pdl_enter();
   for (int i = 0; i < q.n; ++i) {
     const unsigned long long v = *q.seq[i] + 1;
     *q.seq[i] = v;
@@ -1310,7 +1352,7 @@ void trace_dump(const char* path) {
 }
 
 void launch_signal(unsigned long long* const* flag, unsigned long long* const* seq, int n, cudaStream_t s) {
-  batched(flag, seq, n, [&](const FlagBatch& q) { signal_kernel<<<1, 1, 0, s>>>(q); });
+  batched(flag, seq, n, [&](const FlagBatch& q) { launch_k(signal_kernel, 1, 1, s, true, q); });
 }
 
 void launch_quiesce(const unsigned long long* const* flag, const unsigned long long* const* count, int n,
