@@ -713,33 +713,45 @@ __device__ __forceinline__ void run_put_ll(const DSeg& s, const LaunchParams& P,
   const int64_t lines = (W + 14) / 15;
   const int lane = threadIdx.x & 31;
   const int j = lane & 7;
-  const int64_t L0 = blk * kLLLines + (threadIdx.x >> 5) * (4 * kLLIters) + (lane >> 3);
-  unsigned long long a[kLLIters], b[kLLIters];
+  // One chunk of kLLLines lines starting at the warp's line L0.
+  auto chunk = [&](const int64_t L0) {
+    unsigned long long a[kLLIters], b[kLLIters];
 #pragma unroll
-  for (int u = 0; u < kLLIters; ++u) {
-    const int64_t L = L0 + 4 * u;
-    const int64_t w0 = L * 15 + 2 * j;
-    a[u] = 0;
-    b[u] = m;
-    if (sp.kind == PAT_CONTIG) {  // the common case: one contiguous run of words
-      const unsigned long long* base = src + sp.start * wpv;
-      if (L < lines && w0 < W) a[u] = base[w0];
-      if (L < lines && j != 7 && w0 + 1 < W) b[u] = base[w0 + 1];
-      continue;
+    for (int u = 0; u < kLLIters; ++u) {
+      const int64_t L = L0 + 4 * u;
+      const int64_t w0 = L * 15 + 2 * j;
+      a[u] = 0;
+      b[u] = m;
+      if (sp.kind == PAT_CONTIG) {  // the common case: one contiguous run of words
+        const unsigned long long* base = src + sp.start * wpv;
+        if (L < lines && w0 < W) a[u] = base[w0];
+        if (L < lines && j != 7 && w0 + 1 < W) b[u] = base[w0 + 1];
+        continue;
+      }
+      if (L < lines && w0 < W) {
+        const int64_t i = wpv == 1 ? w0 : w0 / wpv;
+        a[u] = src[pat_index(sp, i) * wpv + (w0 - i * wpv)];
+      }
+      if (L < lines && j != 7 && w0 + 1 < W) {
+        const int64_t i = wpv == 1 ? w0 + 1 : (w0 + 1) / wpv;
+        b[u] = src[pat_index(sp, i) * wpv + (w0 + 1 - i * wpv)];
+      }
     }
-    if (L < lines && w0 < W) {
-      const int64_t i = wpv == 1 ? w0 : w0 / wpv;
-      a[u] = src[pat_index(sp, i) * wpv + (w0 - i * wpv)];
+#pragma unroll
+    for (int u = 0; u < kLLIters; ++u) {
+      const int64_t L = L0 + 4 * u;
+      if (L < lines) st_v2_volatile(dst + L * 16 + 2 * j, a[u], b[u]);
     }
-    if (L < lines && j != 7 && w0 + 1 < W) {
-      const int64_t i = wpv == 1 ? w0 + 1 : (w0 + 1) / wpv;
-      b[u] = src[pat_index(sp, i) * wpv + (w0 + 1 - i * wpv)];
-    }
+  };
+  const int64_t off = (threadIdx.x >> 5) * (4 * kLLIters) + (lane >> 3);
+  if (s.ll_loop <= 1) {
+    chunk(blk * kLLLines + off);
+    return;
   }
-#pragma unroll
-  for (int u = 0; u < kLLIters; ++u) {
-    const int64_t L = L0 + 4 * u;
-    if (L < lines) st_v2_volatile(dst + L * 16 + 2 * j, a[u], b[u]);
+  for (int64_t c = blk * s.ll_loop; c < (blk + 1) * s.ll_loop; ++c) {
+    const int64_t L0 = c * kLLLines + off;
+    if (__all_sync(0xffffffffu, L0 >= lines)) break;
+    chunk(L0);
   }
 }
 
@@ -1200,6 +1212,8 @@ int64_t resident_ctas(ElemType t, int op) {
 int launch_segments(LaunchParams& p, ElemType t, int op, cudaStream_t stream) {
   int64_t blocks = 0;
   int n = 0;
+  bool op_recv = false;  // an LL128 receive applies an op (not a copy)
+  for (int s = 0; s < p.nseg; ++s) op_recv = op_recv || (p.seg[s].type == SEG_RECV_LL && !p.seg[s].replace);
   for (int s = 0; s < p.nseg; ++s) {
     const int64_t items = p.seg[s].n * p.bl;
     if (items <= 0) continue;
@@ -1209,7 +1223,23 @@ int launch_segments(LaunchParams& p, ElemType t, int op, cudaStream_t stream) {
     const bool ll = p.seg[s].type == SEG_PUT_LL || p.seg[s].type == SEG_RECV_LL;
     const int64_t per_block = !csr ? kThreads * kItems : p.seg[n].csr_warp ? kThreads / 32 : kThreads;
     int64_t nb = (items + per_block - 1) / per_block;
-    if (ll) nb = ((p.seg[s].n * p.wpv + 14) / 15 + kLLLines - 1) / kLLLines;
+    if (ll) {
+      // Large puts in a launch whose receives apply an op (a halo Reduce
+      // folding contributions as they land) write two chunks per CTA, which
+      // leaves the receive CTAs more SM slots: 2048^3 halo Reduce at N=2
+      // 79 -> 69 us. A Bcast's copying receives do not gain (66 -> 68 us).
+      const int64_t lines = (p.seg[s].n * p.wpv + 14) / 15;
+      int64_t loop = 1;
+      if (p.seg[s].type == SEG_PUT_LL && lines >= 8192) {
+        static const int64_t put_loop = [] {  // ablation / override
+          const char* e = std::getenv("SFG_LL_PUT_LOOP");
+          return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(0);
+        }();
+        loop = put_loop > 0 ? put_loop : op_recv ? 2 : 1;
+      }
+      p.seg[n].ll_loop = loop;
+      nb = (lines + kLLLines * loop - 1) / (kLLLines * loop);
+    }
     if (csr && p.seg[n].csr_np > 1) {
       // Piece-major walk: every CTA of the segment must be resident at once.
       const int64_t res = resident_ctas(t, op);

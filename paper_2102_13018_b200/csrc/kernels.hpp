@@ -145,6 +145,8 @@ struct DSeg {
   // LL128 put: the peer's acknowledgement count for this channel; message m
   // may overwrite parity m & 1 once it reaches m - 2.
   const unsigned long long* ll_credit = nullptr;
+  // LL128 put: consecutive kLLLines chunks each CTA writes (launch_segments)
+  int64_t ll_loop = 1;
 };
 
 // Wait until *flag >= *count + delta (count: a local message counter).
