@@ -25,6 +25,7 @@
 
 #include "kernels.hpp"
 
+
 namespace sfg {
 namespace {
 
@@ -892,9 +893,13 @@ __device__ __forceinline__ void pdl_enter() {
 // instantiation so the CSR paths do not raise their register allocation.
 // MODE 0: pair segments only (4 CTAs/SM); 1 (FULL): CSR / fetch segments
 // too (3 CTAs/SM); 2: pair + LL128 put/receive segments (2 CTAs/SM: the
-// receive keeps 4 lines x 16 bytes per lane in flight without spilling).
+// receive keeps 4 lines x 16 bytes per lane in flight without spilling);
+// 3: the same for large exchanges at 3 CTAs/SM (80 registers, a 32-byte
+// spill): more put and receive CTAs in flight beat the spill once a launch
+// moves >= kLLWideLines lines (2048^3 halo Bcast at N=2 66.4 -> 57.8 us), not
+// below (512^3: 9.2 -> 9.4 us).
 template <class T, int OP, int MODE>
-__global__ void __launch_bounds__(kThreads, MODE == 0 ? 4 : MODE == 1 ? 3 : 2)
+__global__ void __launch_bounds__(kThreads, MODE == 0 ? 4 : MODE == 1 ? 3 : MODE == 2 ? 2 : 3)
     segments_kernel(const __grid_constant__ LaunchParams P) {
   pdl_enter();
   constexpr bool FULL = MODE == 1;
@@ -1091,8 +1096,19 @@ void launch_t(const LaunchParams& p, int64_t blocks, cudaStream_t st) {
     }
   }
   bool ll = false;
-  for (int s = 0; s < p.nseg; ++s) ll = ll || p.seg[s].type == SEG_PUT_LL || p.seg[s].type == SEG_RECV_LL;
-  if (ll && !full) {
+  int64_t ll_lines = 0;
+  for (int s = 0; s < p.nseg; ++s)
+    if (p.seg[s].type == SEG_PUT_LL || p.seg[s].type == SEG_RECV_LL) {
+      ll = true;
+      ll_lines += (p.seg[s].n * p.wpv + 14) / 15;
+    }
+  static const int64_t wide_lines = [] {  // ablation / override
+    const char* e = std::getenv("SFG_LL_WIDE_LINES");
+    return e ? std::atoll(e) : kLLWideLines;
+  }();
+  if (ll && !full && ll_lines >= wide_lines) {
+    launch_k(segments_kernel<T, OP, 3>, blocks, kThreads, st, true, p);
+  } else if (ll && !full) {
     launch_k(segments_kernel<T, OP, 2>, blocks, kThreads, st, true, p);
   } else if constexpr (OP == OP_REPLACE) {
     launch_k(segments_kernel<T, OP, 0>, blocks, kThreads, st, false, p);

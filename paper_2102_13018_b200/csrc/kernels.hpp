@@ -68,6 +68,7 @@ enum SegType : int32_t {
 // for the acknowledgement of message m-2, which is long done.
 constexpr int kLLIters = 4;                  // line groups per warp
 constexpr int kLLLines = 8 * 4 * kLLIters;  // lines per CTA (256 threads)
+constexpr int64_t kLLWideLines = 65536;    // launches moving more lines run at 3 CTAs/SM
 
 // Buffer slots a segment can address; filled per call.
 enum BufId : int32_t {
