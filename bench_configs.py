@@ -573,13 +573,21 @@ def config3(ctx, args):
                 h = sf.reduce_begin(f, u, leaf, root, sf.ReduceOp.sum, ctx.stream)
                 sf.reduce_end(h)
 
-            for name, fn in (("bcast_replace", bc), ("reduce_sum", rd)):
+            def bc1():  # one-shot forms (the ghost update of a VecScatter)
+                sf.bcast(f, u, root, leaf, sf.ReduceOp.replace, ctx.stream, sync=False)
+
+            def rd1():
+                sf.reduce(f, u, leaf, root, sf.ReduceOp.sum, ctx.stream, sync=False)
+
+            for name, fn, fn1 in (("bcast_replace", bc, bc1), ("reduce_sum", rd, rd1)):
                 ms, byts, rec = ctx.timed(fn, args.steps, args.warmup, flush=False)
                 gms = timed_graph(ctx, fn, args.steps, args.warmup)
+                gms1 = timed_graph(ctx, fn1, args.steps, args.warmup)
                 op_line(ctx, 3, name, ms, byts, rec, {"permuted": permute is not None, "N": N,
                                                        "dims": list(dims), "setup_s": setup_s,
                                                        "ghosts_rank0": int(specs[0].nleaves),
-                                                       "graph_us_per_op": gms * 1e3})
+                                                       "graph_us_per_op": gms * 1e3,
+                                                       "graph_us_per_op_one_shot": gms1 * 1e3})
             continue
         if ctx.rank != 0:
             continue
