@@ -1246,13 +1246,12 @@ int launch_segments(LaunchParams& p, ElemType t, int op, cudaStream_t stream) {
       // 79 -> 69 us. A Bcast's copying receives do not gain (66 -> 68 us).
       const int64_t lines = (p.seg[s].n * p.wpv + 14) / 15;
       int64_t loop = 1;
-      if (p.seg[s].type == SEG_PUT_LL && lines >= 8192) {
-        static const int64_t put_loop = [] {  // ablation / override
-          const char* e = std::getenv("SFG_LL_PUT_LOOP");
-          return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(0);
-        }();
-        loop = put_loop > 0 ? put_loop : op_recv ? 2 : 1;
-      }
+      static const int64_t put_loop = [] {  // ablation / override (any size)
+        const char* e = std::getenv("SFG_LL_PUT_LOOP");
+        return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t(0);
+      }();
+      if (p.seg[s].type == SEG_PUT_LL)
+        loop = put_loop > 0 ? put_loop : op_recv && lines >= 8192 ? 2 : 1;
       p.seg[n].ll_loop = loop;
       nb = (lines + kLLLines * loop - 1) / (kLLLines * loop);
     }

@@ -272,6 +272,23 @@ def test_process_per_gpu_torchrun(backend):
     assert "mp_worker ok" in r.stdout
 
 
+@need2
+def test_process_per_gpu_wide_exchange_paths():
+    """The large-exchange paths on small forests, forced through their
+    switches (read once per process, hence a fresh torchrun): every LL128
+    launch on the 3-CTA/SM instantiation (SFG_LL_WIDE_LINES=0) and every put
+    writing several chunks per CTA (SFG_LL_PUT_LOOP=3); p2p results against
+    the oracle as in test_process_per_gpu_torchrun."""
+    n = min(ngpu(), 4)
+    env = dict(os.environ, SFG_LL_WIDE_LINES="0", SFG_LL_PUT_LOOP="3")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port",
+                        "29537", os.path.join(ROOT, "tests", "mp_worker.py"), "p2p"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "mp_worker ok" in r.stdout
+
+
 def _counted(specs, opkind, data, op, backend, n):
     sf.counters_reset()
     run_gpu(specs, opkind, data, op=op, config=sf.CommConfig(backend=backend), devices=list(range(n)))
