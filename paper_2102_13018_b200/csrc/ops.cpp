@@ -397,6 +397,7 @@ struct Launch {
           q.push_back(d.seq);
         }
         launch_signal(f.data(), q.data(), static_cast<int>(f.size()), st);
+        SFG_CUDA(cudaGetLastError());
         ++launched;
       }
     }
